@@ -1,0 +1,346 @@
+// abi.cu -- the C-ABI declared in include/bicount_b200.h.
+//
+// bc_count replaces the reference's count_bicliques (engine.py:419-500):
+// validate like EngineConfig.validate / _build_shared (engine.py:53-61,
+// 387-391), upload the CSR, run preprocessing (prep.cu) and the search
+// (search.cu), and return the exact count and CountReport fields.
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "engine.h"
+
+namespace bc {
+thread_local int64_t t_h2d_bytes = 0, t_d2h_bytes = 0;
+}
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_mu;  // serialise calls (one Python thread drives the library)
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+__global__ void degree_stats(const int64_t *off, int64_t n, unsigned long long *wedge,
+                             int *maxdeg) {
+  unsigned long long w = 0;
+  int md = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = off[i + 1] - off[i];
+    w += (unsigned long long)(d * (d - 1) / 2);
+    md = d > md ? (int)d : md;
+  }
+  w = bc::warp_sum(w);
+  md = __reduce_max_sync(bc::FULL, (unsigned)md);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(wedge, w);
+    atomicMax(maxdeg, md);
+  }
+}
+
+void validate_config(const bc_config &c) {
+  using bc::Error;
+  if (c.batch_words < 1) throw Error(BC_EINVAL, "batch_buffer_capacity must be >= 1");
+  if (c.mode != 0 && c.mode != 1) throw Error(BC_EINVAL, "mode must be one of ('dfs', 'hybrid')");
+  if (c.anchor < -1 || c.anchor > 1) throw Error(BC_EINVAL, "anchor must be one of ('auto', 'U', 'V')");
+  if (c.shard_count < 1 || c.shard_index < 0 || c.shard_index >= c.shard_count)
+    throw Error(BC_EINVAL, "invalid shard_index / shard_count");
+  if (c.order_mode != 0) throw Error(BC_EINVAL, "order_mode must be 0 (reference)");
+}
+
+void fill_from_structs(const bc::DevStructs &s, bc_report &out) {
+  out.anchor = s.anchor;
+  out.p_eff = s.p_eff;
+  out.q_eff = s.q_eff;
+  out.tasks_emitted = s.emitted;
+  out.roots_filtered = s.filtered;
+  out.und_pairs = s.und_pairs;
+  out.dir2_pairs = s.dir2_pairs;
+  out.adj_words = s.adj_words;
+  out.dir2_words = s.dir2_words;
+  out.max_slice_words = s.max_adj_slice > s.max_dir_slice ? s.max_adj_slice : s.max_dir_slice;
+  out.kernel_launches += s.launches;
+}
+
+}  // namespace
+
+struct bc_graph {
+  bc::DevGraph g;
+};
+
+struct bc_structs {
+  bc::DevGraph *g = nullptr;
+  bc::DevStructs s;
+};
+
+extern "C" {
+
+int bc_abi_version(void) { return BC_ABI_VERSION; }
+
+const char *bc_last_error(void) { return g_err.c_str(); }
+
+int bc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
+                    const int64_t *v_off, const int32_t *v_idx, int64_t n_v, int32_t device,
+                    bc_graph **out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  *out = nullptr;
+  if (n_u < 0 || n_v < 0 || !u_off || !v_off) return fail(BC_EINVAL, "invalid graph arrays");
+  if (n_u >= (int64_t(1) << 31) || n_v >= (int64_t(1) << 31))
+    return fail(BC_EINVAL, "layer sizes must be < 2^31");
+  const int64_t e = u_off[n_u];
+  if (v_off[n_v] != e) return fail(BC_EINVAL, "U and V views disagree on the edge count");
+  bc_graph *h = new bc_graph();
+  try {
+    bc::DevGraph &g = h->g;
+    g.device = device;
+    BC_CUDA(cudaSetDevice(device));
+    BC_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    g.n_u = n_u;
+    g.n_v = n_v;
+    g.n_e = e;
+    cudaStream_t st = g.stream;
+    BC_CUDA(cudaMallocAsync((void **)&g.u_off, (n_u + 1) * 8, st));
+    BC_CUDA(cudaMallocAsync((void **)&g.v_off, (n_v + 1) * 8, st));
+    BC_CUDA(cudaMallocAsync((void **)&g.u_idx, (e ? e : 1) * 4, st));
+    BC_CUDA(cudaMallocAsync((void **)&g.v_idx, (e ? e : 1) * 4, st));
+    bc::copy_h2d(g.u_off, u_off, (n_u + 1) * 8, st);
+    bc::copy_h2d(g.v_off, v_off, (n_v + 1) * 8, st);
+    if (e) {
+      bc::copy_h2d(g.u_idx, u_idx, e * 4, st);
+      bc::copy_h2d(g.v_idx, v_idx, e * 4, st);
+    }
+    // wedge mass + max degree per layer (graph.py:246-249), once per graph
+    unsigned long long *dw;
+    int *dm;
+    BC_CUDA(cudaMallocAsync((void **)&dw, 16, st));
+    BC_CUDA(cudaMallocAsync((void **)&dm, 8, st));
+    BC_CUDA(cudaMemsetAsync(dw, 0, 16, st));
+    BC_CUDA(cudaMemsetAsync(dm, 0, 8, st));
+    const int sms = bc::num_sms(device);
+    degree_stats<<<sms * 4, 256, 0, st>>>(g.u_off, n_u, dw, dm);
+    degree_stats<<<sms * 4, 256, 0, st>>>(g.v_off, n_v, dw + 1, dm + 1);
+    BC_CHECK_LAUNCH();
+    unsigned long long hw[2];
+    int hm[2];
+    bc::copy_d2h(hw, dw, 16, st);
+    bc::copy_d2h(hm, dm, 8, st);
+    BC_CUDA(cudaFreeAsync(dw, st));
+    BC_CUDA(cudaFreeAsync(dm, st));
+    BC_CUDA(cudaStreamSynchronize(st));
+    g.wedge_u = (int64_t)hw[0];
+    g.wedge_v = (int64_t)hw[1];
+    g.max_deg_u = hm[0];
+    g.max_deg_v = hm[1];
+  } catch (const bc::Error &err) {
+    bc_graph_destroy(h);
+    return fail(err.code, err.what());
+  }
+  *out = h;
+  return BC_OK;
+}
+
+void bc_graph_destroy(bc_graph *h) {
+  if (!h) return;
+  bc::DevGraph &g = h->g;
+  cudaSetDevice(g.device);
+  if (g.stream) {
+    cudaFreeAsync(g.u_off, g.stream);
+    cudaFreeAsync(g.v_off, g.stream);
+    cudaFreeAsync(g.u_idx, g.stream);
+    cudaFreeAsync(g.v_idx, g.stream);
+    cudaStreamSynchronize(g.stream);
+    cudaStreamDestroy(g.stream);
+  }
+  delete h;
+}
+
+static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_report *out) {
+  try {
+    if (!h || !cfg || !out) throw bc::Error(BC_EINVAL, "null argument");
+    validate_config(*cfg);
+    if (p < 1 || q < 1) throw bc::Error(BC_EINVAL, "p and q must be >= 1");
+    BC_CUDA(cudaSetDevice(h->g.device));
+    const double t0 = now_s();
+    bc::DevStructs s;
+    cudaEvent_t a, b;
+    BC_CUDA(cudaEventCreate(&a));
+    BC_CUDA(cudaEventCreate(&b));
+    BC_CUDA(cudaEventRecord(a, h->g.stream));
+    bc::prepare(h->g, p, q, *cfg, s);
+    BC_CUDA(cudaEventRecord(b, h->g.stream));
+    // _build_shared capacity check (engine.py:382-391)
+    const int64_t max_words = s.max_adj_slice > s.max_dir_slice ? s.max_adj_slice : s.max_dir_slice;
+    if (cfg->batch_words < max_words)
+      throw bc::Error(BC_EINVAL, "batch_buffer_capacity " + std::to_string(cfg->batch_words) +
+                                     " words is below the largest candidate slice (" +
+                                     std::to_string(max_words) +
+                                     " words); raise --batch-words");
+    fill_from_structs(s, *out);
+    bc::search(s, *cfg, *out);
+    float ms = 0;
+    BC_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    out->time_prep = ms * 1e-3;
+    out->time_total = now_s() - t0;
+    if (out->overflow) throw bc::Error(BC_EOVERFLOW, "biclique count exceeds 128 bits");
+  } catch (const bc::Error &err) {
+    cudaStreamSynchronize(h ? h->g.stream : 0);
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
+}
+
+int bc_graph_count(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_report *out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  if (out) std::memset(out, 0, sizeof *out);
+  bc::t_h2d_bytes = bc::t_d2h_bytes = 0;
+  const int rc = count_impl(h, p, q, cfg, out);
+  if (out) {
+    out->h2d_bytes = bc::t_h2d_bytes;
+    out->d2h_bytes = bc::t_d2h_bytes;
+  }
+  return rc;
+}
+
+int bc_count(const int64_t *u_off, const int32_t *u_idx, int64_t n_u, const int64_t *v_off,
+             const int32_t *v_idx, int64_t n_v, int32_t p, int32_t q, const bc_config *cfg,
+             bc_report *out) {
+  if (out) std::memset(out, 0, sizeof *out);
+  const double t0 = now_s();
+  bc_graph *h = nullptr;
+  bc::t_h2d_bytes = bc::t_d2h_bytes = 0;
+  int rc = bc_graph_create(u_off, u_idx, n_u, v_off, v_idx, n_v, cfg ? cfg->device : 0, &h);
+  if (rc != BC_OK) return rc;
+  const double t1 = now_s();
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_err.clear();
+    rc = count_impl(h, p, q, cfg, out);
+  }
+  const double t2 = now_s();
+  bc_graph_destroy(h);
+  if (out) {
+    out->time_h2d = t1 - t0;
+    out->time_total = now_s() - t0;
+    out->h2d_bytes = bc::t_h2d_bytes;
+    out->d2h_bytes = bc::t_d2h_bytes;
+    (void)t2;
+  }
+  return rc;
+}
+
+int bc_prepare(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_structs **out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  *out = nullptr;
+  bc_structs *r = new bc_structs();
+  try {
+    if (!h || !cfg) throw bc::Error(BC_EINVAL, "null argument");
+    validate_config(*cfg);
+    BC_CUDA(cudaSetDevice(h->g.device));
+    r->g = &h->g;
+    bc::prepare(h->g, p, q, *cfg, r->s);
+    BC_CUDA(cudaStreamSynchronize(h->g.stream));
+  } catch (const bc::Error &err) {
+    delete r;
+    return fail(err.code, err.what());
+  }
+  *out = r;
+  return BC_OK;
+}
+
+int64_t bc_export_len(const bc_structs *r, int32_t what) {
+  if (!r) return -1;
+  const bc::DevStructs &s = r->s;
+  const int64_t n = s.n;
+  switch (what) {
+    case BC_X_UND_SIZE:
+    case BC_X_RANK:
+    case BC_X_ORDER: return n;
+    case BC_X_DIR_OFF:
+    case BC_X_HADJ_OFF:
+    case BC_X_HDIR_OFF: return n + 1;
+    case BC_X_DIR_IDX: return s.dir2_pairs;
+    case BC_X_HADJ_IDX:
+    case BC_X_HADJ_VAL: return s.adj_words;
+    case BC_X_HDIR_IDX:
+    case BC_X_HDIR_VAL: return s.dir2_words;
+    case BC_X_TASKS: return 2 * s.emitted;
+    case BC_X_META: return 4;
+  }
+  return -1;
+}
+
+int bc_export(const bc_structs *r, int32_t what, void *dst) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  try {
+    if (!r || !dst) throw bc::Error(BC_EINVAL, "null argument");
+    const bc::DevStructs &s = r->s;
+    BC_CUDA(cudaSetDevice(r->g->device));
+    const int64_t len = bc_export_len(r, what);
+    if (len < 0) throw bc::Error(BC_EINVAL, "unknown export id");
+    const void *src = nullptr;
+    size_t el = 8;
+    switch (what) {
+      case BC_X_UND_SIZE: src = s.und_size.p; break;
+      case BC_X_RANK: src = s.rank.p; break;
+      case BC_X_ORDER: src = s.order.p; break;
+      case BC_X_DIR_OFF: src = s.dir_off.p; break;
+      case BC_X_DIR_IDX: src = s.dir_idx.p; el = 4; break;
+      case BC_X_HADJ_OFF: src = s.hadj_off.p; break;
+      case BC_X_HADJ_IDX: src = s.hadj_idx.p; el = 4; break;
+      case BC_X_HADJ_VAL: src = s.hadj_val.p; el = 4; break;
+      case BC_X_HDIR_OFF: src = s.hdir_off.p; break;
+      case BC_X_HDIR_IDX: src = s.hdir_idx.p; el = 4; break;
+      case BC_X_HDIR_VAL: src = s.hdir_val.p; el = 4; break;
+      case BC_X_TASKS: src = s.tasks.p; el = 4; break;
+      case BC_X_META: {
+        int64_t *d = (int64_t *)dst;
+        d[0] = s.anchor; d[1] = s.p_eff; d[2] = s.q_eff; d[3] = s.n;
+        return BC_OK;
+      }
+    }
+    if (len > 0) {
+      bc::copy_d2h(dst, src, (size_t)len * el, s.stream);
+      BC_CUDA(cudaStreamSynchronize(s.stream));
+    }
+  } catch (const bc::Error &err) {
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
+}
+
+void bc_structs_destroy(bc_structs *r) {
+  if (!r) return;
+  cudaSetDevice(r->g->device);
+  cudaStream_t st = r->s.stream;
+  delete r;  // DBuf destructors free stream-ordered
+  if (st) cudaStreamSynchronize(st);
+}
+
+void bc_shutdown(void) {}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// engine.h -- host-side orchestration types shared by prep.cu, search.cu, abi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace bc {
+
+// Device-resident CSR of both views (BipartiteGraph, graph.py:15-49).
+struct DevGraph {
+  int device = 0;
+  int64_t n_u = 0, n_v = 0, n_e = 0;
+  int64_t *u_off = nullptr;
+  int32_t *u_idx = nullptr;
+  int64_t *v_off = nullptr;
+  int32_t *v_idx = nullptr;
+  cudaStream_t stream = nullptr;
+  int max_deg_u = 0, max_deg_v = 0;
+  int64_t wedge_u = 0, wedge_v = 0;  // sum C(d,2) per layer (graph.py:246-249)
+};
+
+// Stream-ordered device buffer.
+template <typename T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept { *this = std::move(o); }
+  DBuf &operator=(DBuf &&o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    BC_CUDA(cudaMallocAsync((void **)&p, (count ? count : 1) * sizeof(T), stream));
+  }
+  void zero() { if (n) BC_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+};
+
+// Host<->device traffic of the current call (reported in bc_report).
+extern thread_local int64_t t_h2d_bytes, t_d2h_bytes;
+
+inline void copy_h2d(void *dst, const void *src, size_t n, cudaStream_t st) {
+  if (!n) return;
+  BC_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+  t_h2d_bytes += (int64_t)n;
+}
+
+inline void copy_d2h(void *dst, const void *src, size_t n, cudaStream_t st) {
+  if (!n) return;
+  BC_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+  t_d2h_bytes += (int64_t)n;
+}
+
+// Prepared structures on device (SearchStructures, engine.py:82-92).
+struct DevStructs {
+  int anchor = 0, p_eff = 0, q_eff = 0;
+  int64_t n = 0, m = 0;  // anchor-layer and opposite-layer sizes
+  // borrowed from DevGraph: work.u_adj / work.v_adj (engine.py:126)
+  const int64_t *aoff = nullptr;
+  const int32_t *aidx = nullptr;
+  const int64_t *boff = nullptr;
+  const int32_t *bidx = nullptr;
+  int max_deg_anchor = 0;
+  DBuf<int64_t> und_size, rank, order;
+  DBuf<int64_t> dir_off;
+  DBuf<int32_t> dir_idx;
+  DBuf<int64_t> hadj_off, hdir_off;
+  DBuf<uint32_t> hadj_idx, hadj_val, hdir_idx, hdir_val;
+  DBuf<int2> tasks;  // (root, second) in emission order
+  int64_t emitted = 0, filtered = 0;
+  int64_t und_pairs = 0, dir2_pairs = 0, adj_words = 0, dir2_words = 0;
+  int64_t max_adj_slice = 0, max_dir_slice = 0;
+  int64_t launches = 0;
+  cudaStream_t stream = nullptr;
+};
+
+// Preprocessing: anchor choice .. task emission (prep.cu).
+void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s);
+
+// Enumeration: level-1 pass + hybrid search (search.cu). Fills counters in out.
+void search(const DevStructs &s, const bc_config &cfg, bc_report &out);
+
+int num_sms(int device);
+
+}  // namespace bc

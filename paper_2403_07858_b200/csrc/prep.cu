@@ -1,0 +1,565 @@
+// prep.cu -- device preprocessing for the (p,q)-biclique path (sm_100a).
+//
+// Restates, on device, prepare_structures (reference engine.py:115-144) and
+// pre_runtime_tasks (engine.py:147-173):
+//   anchor choice    graph.py:246-269   wedge mass per layer (computed at graph upload)
+//   2-hop index      graph.py:192-215   CTA per anchor vertex, packed u16 counters in smem
+//   priority         graph.py:227-243   radix sort on (|N2|, id)
+//   directed filter  graph.py:218-224   warp per vertex, order-preserving ballot compaction
+//   HTB              htb.py:89-115      warp per set, run boundaries by ballot
+//   tasks            engine.py:147-173  scan over the priority order
+// Every array is bit-identical to the reference's (tests/test_gpu_parity.py).
+#include <cub/cub.cuh>
+
+#include "engine.h"
+
+namespace bc {
+
+namespace {
+
+template <typename T>
+void exclusive_scan(const T *in, T *out, int64_t n, cudaStream_t st) {
+  size_t tmp = 0;
+  BC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
+  DBuf<char> t;
+  t.alloc(tmp, st);
+  BC_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, st));
+}
+
+template <typename T>
+T d2h_scalar(const T *p, cudaStream_t st) {
+  T v;
+  copy_d2h(&v, p, sizeof(T), st);
+  BC_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// 2-hop index: one CTA per anchor vertex u (dynamic queue, heaviest first).
+// Counters for ids of the current tile live in shared memory (two u16 per
+// u32 word, or one u32 per id when WIDE).  Increments stop once a counter
+// reaches k (the reads are racy but monotone, so a stale read only costs one
+// extra increment; at most blockDim extra increments per id keep u16 safe).
+// The kept ids (count >= k, != u) are emitted in ascending order by scanning
+// the counter tile, which also zeroes it for the next vertex.
+// ---------------------------------------------------------------------------
+constexpr int TH_THREADS = 512;
+
+template <bool WIDE>
+__device__ __forceinline__ uint32_t ctr_get(const uint32_t *c, int64_t i) {
+  if (WIDE) return c[i];
+  return (c[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+}
+
+template <bool WIDE>
+__global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
+    const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
+    const int64_t *__restrict__ boff, const int32_t *__restrict__ bidx,
+    const int32_t *__restrict__ vorder, int64_t n, uint32_t k, int64_t tile, int ntiles,
+    int *next, int64_t *__restrict__ und_size, int64_t *__restrict__ seg_start,
+    int32_t *__restrict__ seg_len, int32_t *__restrict__ out_ids, int64_t out_cap,
+    unsigned long long *out_used, int *overflow) {
+  extern __shared__ uint32_t ctr[];
+  __shared__ int64_t s_u;
+  __shared__ int s_warp[TH_THREADS / 32];
+  __shared__ int64_t s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = TH_THREADS / 32;
+  const int64_t nwords = WIDE ? tile : (tile + 1) / 2;
+  for (int64_t i = tid; i < nwords; i += TH_THREADS) ctr[i] = 0;
+  __syncthreads();
+  for (;;) {
+    if (tid == 0) {
+      int j = atomicAdd(next, 1);
+      s_u = j < n ? vorder[j] : -1;
+    }
+    __syncthreads();
+    const int64_t u = s_u;
+    if (u < 0) break;
+    const int64_t e0 = aoff[u], e1 = aoff[u + 1];
+    int64_t total = 0;
+    for (int ti = 0; ti < ntiles; ti++) {
+      const int64_t t0 = (int64_t)ti * tile;
+      const int64_t t1 = t0 + tile < n ? t0 + tile : n;
+      // count phase: warp per 1-hop neighbour v, lanes stride N(v)
+      for (int64_t e = e0 + warp; e < e1; e += nwarps) {
+        const int32_t v = __ldg(aidx + e);
+        const int64_t f0 = __ldg(boff + v), f1 = __ldg(boff + v + 1);
+        for (int64_t f = f0 + lane; f < f1; f += 32) {
+          const int64_t w = __ldg(bidx + f);
+          if (w < t0 || w >= t1) continue;
+          const int64_t l = w - t0;
+          if (WIDE) {
+            if (((volatile uint32_t *)ctr)[l] < k) atomicAdd(&ctr[l], 1u);
+          } else {
+            const int sh = (int)(l & 1) * 16;
+            uint32_t c = (((volatile uint32_t *)ctr)[l >> 1] >> sh) & 0xffffu;
+            if (c < k) atomicAdd(&ctr[l >> 1], 1u << sh);
+          }
+        }
+      }
+      __syncthreads();
+      // kept-count phase
+      const int64_t len = t1 - t0;
+      int mine = 0;
+      for (int64_t l = tid; l < len; l += TH_THREADS)
+        mine += (ctr_get<WIDE>(ctr, l) >= k && t0 + l != u) ? 1 : 0;
+      mine = __reduce_add_sync(FULL, mine);
+      if (lane == 0) s_warp[warp] = mine;
+      __syncthreads();
+      if (tid == 0) {
+        int64_t kept = 0;
+        for (int w = 0; w < nwarps; w++) kept += s_warp[w];
+        int64_t base = -1;
+        if (kept) {
+          unsigned long long b = atomicAdd(out_used, (unsigned long long)kept);
+          if ((int64_t)b + kept > out_cap) atomicExch(overflow, 1);
+          else base = (int64_t)b;
+        }
+        s_base = base;
+        seg_start[u * ntiles + ti] = base;
+        seg_len[u * ntiles + ti] = (int32_t)kept;
+        s_warp[0] = (int)kept;
+      }
+      __syncthreads();
+      total += s_warp[0];
+      const int64_t base = s_base;
+      __syncthreads();
+      // write phase (ascending ids, order-preserving) + zero the tile
+      int64_t pos = 0;
+      for (int64_t c0 = 0; c0 < len; c0 += TH_THREADS) {
+        const int64_t l = c0 + tid;
+        bool keep = false;
+        if (l < len) keep = ctr_get<WIDE>(ctr, l) >= k && t0 + l != u;
+        const unsigned b = __ballot_sync(FULL, keep);
+        if (lane == 0) s_warp[warp] = __popc(b);
+        __syncthreads();
+        int before = 0, all = 0;
+        for (int w = 0; w < nwarps; w++) {
+          int c = s_warp[w];
+          before += (w < warp) ? c : 0;
+          all += c;
+        }
+        if (keep && base >= 0) out_ids[base + pos + before + __popc(b & lanemask_lt())] = (int32_t)(t0 + l);
+        pos += all;
+        __syncthreads();
+      }
+      for (int64_t i = tid; i < (WIDE ? len : (len + 1) / 2); i += TH_THREADS) ctr[i] = 0;
+      __syncthreads();
+    }
+    if (tid == 0) und_size[u] = total;
+    __syncthreads();
+  }
+}
+
+// vertices by descending degree (LPT order for the 2-hop CTAs)
+__global__ void degree_keys(const int64_t *off, int64_t n, unsigned long long *keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
+    keys[i] = ((~d & 0xffffffffull) << 32) | (unsigned long long)i;  // ascending key = descending degree
+  }
+}
+
+__global__ void low_bits(const unsigned long long *keys, int64_t n, int32_t *out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)(keys[i] & 0xffffffffull);
+}
+
+// vertex_priority (graph.py:227-243): ascending (size, id) -> rank n..1
+__global__ void priority_keys(const int64_t *size, int64_t n, unsigned long long *keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((unsigned long long)size[i] << 32) | (unsigned long long)i;
+}
+
+__global__ void priority_rank(const unsigned long long *sorted, int64_t n, int64_t *rank,
+                              int64_t *order) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    int64_t id = (int64_t)(sorted[i] & 0xffffffffull);
+    order[i] = id;
+    rank[id] = n - i;
+  }
+}
+
+__global__ void iota64(int64_t *a, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+__global__ void adjacent_dupes(const int64_t *sorted, int64_t n, int *flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > 0 && i < n && sorted[i] == sorted[i - 1]) atomicExch(flag, 1);
+}
+
+// directed_from_undirected (graph.py:218-224): keep rank[w] < rank[u], order kept.
+template <bool WRITE>
+__global__ void directed_filter(const int64_t *__restrict__ seg_start,
+                                const int32_t *__restrict__ seg_len, int ntiles,
+                                const int32_t *__restrict__ und_ids,
+                                const int64_t *__restrict__ rank, int64_t n,
+                                int64_t *__restrict__ dir_size, const int64_t *__restrict__ dir_off,
+                                int32_t *__restrict__ dir_idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n; u += nw) {
+    const int64_t ru = rank[u];
+    int64_t pos = WRITE ? dir_off[u] : 0;
+    for (int ti = 0; ti < ntiles; ti++) {
+      const int64_t st = seg_start[u * ntiles + ti];
+      const int32_t ln = seg_len[u * ntiles + ti];
+      for (int32_t b = 0; b < ln; b += 32) {
+        bool keep = false;
+        int32_t w = 0;
+        if (b + lane < ln) {
+          w = und_ids[st + b + lane];
+          keep = __ldg(rank + w) < ru;
+        }
+        const unsigned m = __ballot_sync(FULL, keep);
+        if (WRITE && keep) dir_idx[pos + __popc(m & lanemask_lt())] = w;
+        pos += __popc(m);
+      }
+    }
+    if (!WRITE && lane == 0) dir_size[u] = pos;
+  }
+}
+
+// HTB (htb.py:89-115): per set, idx = distinct id>>5, val = OR of 1<<(id&31).
+template <bool WRITE>
+__global__ void htb_build(const int64_t *__restrict__ off, const int32_t *__restrict__ idx,
+                          int64_t n, int64_t *__restrict__ words, const int64_t *__restrict__ hoff,
+                          uint32_t *__restrict__ hidx, uint32_t *__restrict__ hval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n; u += nw) {
+    const int64_t a = off[u], b = off[u + 1];
+    int64_t pos = WRITE ? hoff[u] : 0;
+    for (int64_t c = a; c < b; c += 32) {
+      const int64_t i = c + lane;
+      bool start = false;
+      uint32_t word = 0;
+      if (i < b) {
+        word = (uint32_t)__ldg(idx + i) >> 5;
+        start = (i == a) || (((uint32_t)__ldg(idx + i - 1) >> 5) != word);
+      }
+      const unsigned m = __ballot_sync(FULL, start);
+      if (WRITE && start) {
+        uint32_t v = 0;
+        for (int64_t j = i; j < b; j++) {
+          const uint32_t id = (uint32_t)__ldg(idx + j);
+          if ((id >> 5) != word) break;
+          v |= 1u << (id & 31);
+        }
+        const int64_t o = pos + __popc(m & lanemask_lt());
+        hidx[o] = word;
+        hval[o] = v;
+      }
+      pos += __popc(m);
+    }
+    if (!WRITE && lane == 0) words[u] = pos - (WRITE ? hoff[u] : 0);
+  }
+}
+
+__global__ void set_mask(const int32_t *roots, int64_t nr, int64_t n, uint8_t *mask) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nr) {
+    int64_t r = roots[i];
+    if (r >= 0 && r < n) mask[r] = 1;
+  }
+}
+
+// pre_runtime_tasks (engine.py:147-173): per priority position, task count.
+__global__ void task_counts(const int64_t *__restrict__ order, const int64_t *__restrict__ und_size,
+                            const int64_t *__restrict__ dir_off, const uint8_t *__restrict__ mask,
+                            int64_t n, int p_eff, int64_t *__restrict__ cnt,
+                            unsigned long long *filtered) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = order[i];
+  int64_t c = 0;
+  if (!mask || mask[r]) {
+    if (und_size[r] < p_eff - 1) atomicAdd(filtered, 1ull);
+    else c = p_eff == 1 ? 1 : dir_off[r + 1] - dir_off[r];
+  }
+  cnt[i] = c;
+}
+
+__global__ void task_write(const int64_t *__restrict__ order, const int64_t *__restrict__ toff,
+                           const int64_t *__restrict__ cnt, const int64_t *__restrict__ dir_off,
+                           const int32_t *__restrict__ dir_idx, int64_t n, int p_eff,
+                           int2 *__restrict__ tasks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < n; i += nw) {
+    const int64_t c = cnt[i];
+    if (!c) continue;
+    const int32_t r = (int32_t)order[i];
+    const int64_t o = toff[i];
+    if (p_eff == 1) {
+      if (lane == 0) tasks[o] = make_int2(r, -1);
+      continue;
+    }
+    const int64_t d0 = dir_off[r];
+    for (int64_t j = lane; j < c; j += 32) tasks[o + j] = make_int2(r, dir_idx[d0 + j]);
+  }
+}
+
+__global__ void max_reduce(const int64_t *a, int64_t n, unsigned long long *out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long v = i < n ? (unsigned long long)a[i] : 0;
+  v = __reduce_max_sync(FULL, (unsigned)v);  // words per slice < 2^32
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
+inline unsigned blocks_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+inline unsigned warp_blocks(int64_t n_items, int sms) {
+  int64_t b = (n_items * 32 + 255) / 256;
+  int64_t cap = (int64_t)sms * 16;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// HTB of a CSR family into (off, idx, val)
+void build_htb(const int64_t *off, const int32_t *idx, int64_t n, DBuf<int64_t> &hoff,
+               DBuf<uint32_t> &hidx, DBuf<uint32_t> &hval, int64_t &total, int64_t &max_slice,
+               int sms, cudaStream_t st, int64_t &launches) {
+  DBuf<int64_t> words;
+  words.alloc(n + 1, st);
+  words.zero();
+  htb_build<false><<<warp_blocks(n, sms), 256, 0, st>>>(off, idx, n, words.p, nullptr, nullptr,
+                                                      nullptr);
+  BC_CHECK_LAUNCH();
+  hoff.alloc(n + 1, st);
+  exclusive_scan(words.p, hoff.p, n + 1, st);
+  DBuf<unsigned long long> mx;
+  mx.alloc(1, st);
+  mx.zero();
+  max_reduce<<<blocks_for(n, 256), 256, 0, st>>>(words.p, n, mx.p);
+  BC_CHECK_LAUNCH();
+  total = d2h_scalar(hoff.p + n, st);
+  max_slice = (int64_t)d2h_scalar(mx.p, st);
+  hidx.alloc(total, st);
+  hval.alloc(total, st);
+  htb_build<true><<<warp_blocks(n, sms), 256, 0, st>>>(off, idx, n, nullptr, hoff.p, hidx.p,
+                                                     hval.p);
+  BC_CHECK_LAUNCH();
+  launches += 4;
+}
+
+}  // namespace
+
+int num_sms(int device) {
+  int v = 0;
+  BC_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  return v;
+}
+
+void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s) {
+  if (p < 1 || q < 1) throw Error(BC_EINVAL, "p and q must be >= 1");
+  cudaStream_t st = g.stream;
+  s.stream = st;
+  const int sms = num_sms(g.device);
+  int64_t &L = s.launches;
+  // select_anchor_layer (graph.py:252-269): U iff wedge(V) <= wedge(U); V swaps p, q
+  int layer;
+  if (cfg.anchor < 0) layer = g.wedge_v <= g.wedge_u ? 0 : 1;
+  else if (cfg.anchor <= 1) layer = cfg.anchor;
+  else throw Error(BC_EINVAL, "anchor must be one of ('auto', 'U', 'V')");
+  s.anchor = layer;
+  s.p_eff = layer == 0 ? p : q;
+  s.q_eff = layer == 0 ? q : p;
+  s.n = layer == 0 ? g.n_u : g.n_v;
+  s.m = layer == 0 ? g.n_v : g.n_u;
+  s.aoff = layer == 0 ? g.u_off : g.v_off;
+  s.aidx = layer == 0 ? g.u_idx : g.v_idx;
+  s.boff = layer == 0 ? g.v_off : g.u_off;
+  s.bidx = layer == 0 ? g.v_idx : g.u_idx;
+  s.max_deg_anchor = layer == 0 ? g.max_deg_u : g.max_deg_v;
+  const int64_t n = s.n;
+  if (cfg.rank_override && cfg.n_rank != n)
+    throw Error(BC_EINVAL, "rank override must give one distinct value per anchor vertex");
+
+  // ---- 2-hop index, k = q_eff (engine.py:127) ----
+  s.und_size.alloc(n ? n : 1, st);
+  s.und_size.zero();
+  const uint32_t k = (uint32_t)s.q_eff;
+  const bool wide = k > 60000;
+  int ntiles = 1;
+  int64_t tile = n ? n : 1;
+  DBuf<int64_t> seg_start;
+  DBuf<int32_t> seg_len;
+  DBuf<int32_t> und_ids;
+  if (n > 0 && (int64_t)k <= s.max_deg_anchor) {
+    int smem_optin = 0;
+    BC_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g.device));
+    const int64_t max_words = (smem_optin - 4096) / 4;
+    const int64_t max_tile = wide ? max_words : 2 * max_words;
+    ntiles = (int)((n + max_tile - 1) / max_tile);
+    tile = (n + ntiles - 1) / ntiles;
+    if (!wide) tile = (tile + 1) & ~int64_t(1);
+    const size_t smem = (size_t)(wide ? tile : tile / 2) * 4;
+    auto kern = wide ? twohop_kernel<true> : twohop_kernel<false>;
+    BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH_THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
+    // LPT vertex order: descending anchor degree
+    DBuf<unsigned long long> keys, keys2;
+    keys.alloc(n, st);
+    keys2.alloc(n, st);
+    degree_keys<<<blocks_for(n, 256), 256, 0, st>>>(s.aoff, n, keys.p);
+    size_t tmp = 0;
+    BC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.p, keys2.p, n, 0, 64, st));
+    {
+      DBuf<char> t;
+      t.alloc(tmp, st);
+      BC_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tmp, keys.p, keys2.p, n, 0, 64, st));
+    }
+    DBuf<int32_t> vorder;
+    vorder.alloc(n, st);
+    low_bits<<<blocks_for(n, 256), 256, 0, st>>>(keys2.p, n, vorder.p);
+    L += 3;
+    seg_start.alloc((size_t)n * ntiles, st);
+    seg_len.alloc((size_t)n * ntiles, st);
+    // output capacity: the pool bound, capped; retried exactly on overflow
+    const int64_t pool_cap = std::min<int64_t>((int64_t)n * (n - 1), int64_t(1) << 31);
+    int64_t cap = std::min<int64_t>(pool_cap, std::max<int64_t>(int64_t(1) << 24, 64 * n));
+    DBuf<int> ctrs;  // [0] next vertex, [1] overflow
+    DBuf<unsigned long long> used;
+    ctrs.alloc(2, st);
+    used.alloc(1, st);
+    for (int attempt = 0; attempt < 2; attempt++) {
+      und_ids.alloc(cap, st);
+      ctrs.zero();
+      used.zero();
+      kern<<<sms * per_sm, TH_THREADS, smem, st>>>(s.aoff, s.aidx, s.boff, s.bidx, vorder.p, n, k,
+                                                   tile, ntiles, ctrs.p, s.und_size.p,
+                                                   seg_start.p, seg_len.p, und_ids.p, cap, used.p,
+                                                   ctrs.p + 1);
+      BC_CHECK_LAUNCH();
+      L++;
+      int ovf = d2h_scalar(ctrs.p + 1, st);
+      unsigned long long need = d2h_scalar(used.p, st);
+      s.und_pairs = (int64_t)need;
+      if (!ovf) break;
+      if (attempt == 1) throw Error(BC_ECUDA, "2-hop output overflow after exact resize");
+      cap = (int64_t)need;
+    }
+  } else {
+    s.und_pairs = 0;
+    seg_start.alloc((size_t)(n ? n : 1), st);
+    seg_len.alloc((size_t)(n ? n : 1), st);
+    seg_len.zero();
+    seg_start.zero();
+    und_ids.alloc(1, st);
+    ntiles = 1;
+  }
+
+  // ---- priority (graph.py:227-243) or rank override (engine.py:130-134) ----
+  s.rank.alloc(n ? n : 1, st);
+  s.order.alloc(n ? n : 1, st);
+  if (n > 0) {
+    if (!cfg.rank_override) {
+      DBuf<unsigned long long> keys, sorted;
+      keys.alloc(n, st);
+      sorted.alloc(n, st);
+      priority_keys<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, n, keys.p);
+      size_t tmp = 0;
+      BC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.p, sorted.p, n, 0, 64, st));
+      DBuf<char> t;
+      t.alloc(tmp, st);
+      BC_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tmp, keys.p, sorted.p, n, 0, 64, st));
+      priority_rank<<<blocks_for(n, 256), 256, 0, st>>>(sorted.p, n, s.rank.p, s.order.p);
+      L += 3;
+    } else {
+      copy_h2d(s.rank.p, cfg.rank_override, n * sizeof(int64_t), st);
+      DBuf<int64_t> ids, skeys;
+      ids.alloc(n, st);
+      skeys.alloc(n, st);
+      iota64<<<blocks_for(n, 256), 256, 0, st>>>(ids.p, n);
+      size_t tmp = 0;
+      BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, s.rank.p, skeys.p, ids.p,
+                                                        s.order.p, n, 0, 64, st));
+      DBuf<char> t;
+      t.alloc(tmp, st);
+      BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, s.rank.p, skeys.p, ids.p,
+                                                        s.order.p, n, 0, 64, st));
+      DBuf<int> dup;
+      dup.alloc(1, st);
+      dup.zero();
+      adjacent_dupes<<<blocks_for(n, 256), 256, 0, st>>>(skeys.p, n, dup.p);
+      L += 3;
+      if (d2h_scalar(dup.p, st))
+        throw Error(BC_EINVAL, "rank override must give one distinct value per anchor vertex");
+    }
+  }
+
+  // ---- directed 2-hop lists (graph.py:218-224) ----
+  {
+    DBuf<int64_t> dsize;
+    dsize.alloc(n + 1, st);
+    dsize.zero();
+    if (n > 0)
+      directed_filter<false><<<warp_blocks(n, sms), 256, 0, st>>>(
+          seg_start.p, seg_len.p, ntiles, und_ids.p, s.rank.p, n, dsize.p, nullptr, nullptr);
+    s.dir_off.alloc(n + 1, st);
+    exclusive_scan(dsize.p, s.dir_off.p, n + 1, st);
+    s.dir2_pairs = d2h_scalar(s.dir_off.p + n, st);
+    s.dir_idx.alloc(s.dir2_pairs, st);
+    if (n > 0)
+      directed_filter<true><<<warp_blocks(n, sms), 256, 0, st>>>(
+          seg_start.p, seg_len.p, ntiles, und_ids.p, s.rank.p, n, nullptr, s.dir_off.p,
+          s.dir_idx.p);
+    L += 3;
+  }
+  // ---- HTB encodings (htb.py:104-115) ----
+  build_htb(s.aoff, s.aidx, n, s.hadj_off, s.hadj_idx, s.hadj_val, s.adj_words, s.max_adj_slice,
+            sms, st, L);
+  build_htb(s.dir_off.p, s.dir_idx.p, n, s.hdir_off, s.hdir_idx, s.hdir_val, s.dir2_words,
+            s.max_dir_slice, sms, st, L);
+
+  // ---- tasks (engine.py:147-173) ----
+  {
+    DBuf<uint8_t> mask;
+    if (cfg.roots) {
+      mask.alloc(n ? n : 1, st);
+      mask.zero();
+      if (cfg.n_roots > 0) {
+        DBuf<int32_t> r;
+        r.alloc(cfg.n_roots, st);
+        copy_h2d(r.p, cfg.roots, cfg.n_roots * sizeof(int32_t), st);
+        set_mask<<<blocks_for(cfg.n_roots, 256), 256, 0, st>>>(r.p, cfg.n_roots, n, mask.p);
+        L++;
+      }
+    }
+    DBuf<int64_t> cnt, toff;
+    DBuf<unsigned long long> filt;
+    cnt.alloc(n + 1, st);
+    cnt.zero();
+    toff.alloc(n + 1, st);
+    filt.alloc(1, st);
+    filt.zero();
+    if (n > 0)
+      task_counts<<<blocks_for(n, 256), 256, 0, st>>>(s.order.p, s.und_size.p, s.dir_off.p,
+                                                       cfg.roots ? mask.p : nullptr, n, s.p_eff,
+                                                       cnt.p, filt.p);
+    exclusive_scan(cnt.p, toff.p, n + 1, st);
+    s.emitted = d2h_scalar(toff.p + n, st);
+    s.filtered = (int64_t)d2h_scalar(filt.p, st);
+    s.tasks.alloc(s.emitted, st);
+    if (n > 0 && s.emitted)
+      task_write<<<warp_blocks(n, sms), 256, 0, st>>>(s.order.p, toff.p, cnt.p, s.dir_off.p,
+                                                      s.dir_idx.p, n, s.p_eff, s.tasks.p);
+    L += 3;
+  }
+  (void)p;
+}
+
+}  // namespace bc

@@ -1,0 +1,388 @@
+"""Drop-in counting entry point backed by the sm_100a library.
+
+Mirrors the reference engine surface (``pkg/src/bicount/engine.py``):
+
+* ``EngineConfig`` (engine.py:43-61) — same fields, defaults and
+  ``validate()`` errors, plus device knobs (``device``, ``order_mode``).
+* ``CountReport`` (engine.py:64-79) — same fields; ``device`` carries the
+  library's own measurements (phase times, structure sizes, counters).
+* ``count_bicliques(g, p, q, cfg, *, structures=None, roots=None)``
+  (engine.py:419-500) — exact Python-int count computed on the GPU.
+* ``prepare_structures(g, p, q, anchor="auto", rank=None)``
+  (engine.py:115-144) — built on the GPU, exported back to host arrays.
+
+``worker_count`` is validated exactly as in the reference but does not
+change the device schedule (warps pull tasks from one atomic queue).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from time import perf_counter
+
+import numpy as np
+
+from . import _abi
+from .graph import BipartiteGraph, CsrView, as_csr
+
+MODES = ("dfs", "hybrid")
+ANCHOR_FLAGS = ("auto", "U", "V")
+ORDER_MODES = ("reference",)
+
+
+@dataclass
+class EngineConfig:
+    worker_count: int = 1
+    batch_buffer_capacity: int = 4096  # scratch words per level (reference semantics)
+    mode: str = "hybrid"
+    anchor: str = "auto"
+    enumerate_results: bool = False
+    track_tasks: bool = False
+    check_nesting: bool = False
+    # device knobs (not in the reference)
+    device: int = 0
+    order_mode: str = "reference"
+    instrument: bool = False  # tally reference-equivalent intersections (B_enum)
+
+    def validate(self) -> None:
+        if self.worker_count < 1:
+            raise ValueError("worker_count must be >= 1")
+        if self.batch_buffer_capacity < 1:
+            raise ValueError("batch_buffer_capacity must be >= 1")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}")
+        if self.anchor not in ANCHOR_FLAGS:
+            raise ValueError(f"anchor must be one of {ANCHOR_FLAGS}")
+        if self.order_mode not in ORDER_MODES:
+            raise ValueError(f"order_mode must be one of {ORDER_MODES}")
+        if self.enumerate_results:
+            raise NotImplementedError(
+                "enumerate_results is not provided by the B200 counting path "
+                "(SURVEY 8(f) row 4); use the count")
+
+
+@dataclass
+class CountReport:
+    count: int
+    time_1hop: float
+    time_2hop: float
+    batches_executed: int
+    tasks_stolen: int
+    roots_filtered: int
+    wall_time: float
+    tasks_emitted: int
+    tasks_consumed: int
+    workers: int
+    anchor_layer: str
+    bicliques: list | None = None
+    task_tally: list | None = None
+    task_counts: list | None = None
+    device: dict = field(default_factory=dict)
+
+
+@dataclass
+class AnchorChoice:  # graph.py:76-80
+    layer: str
+    p_eff: int
+    q_eff: int
+
+
+@dataclass
+class PriorityOrder:  # graph.py:67-73
+    rank: np.ndarray
+    order: np.ndarray
+
+
+@dataclass
+class TwoHopIndex:  # graph.py:52-64 (directed lists as CSR)
+    k: int
+    layer: str
+    csr: CsrView
+    directed: bool
+
+    @property
+    def lists(self) -> list[np.ndarray]:
+        return [self.csr.row(i) for i in range(self.csr.n)]
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return self.csr.degrees()
+
+
+@dataclass
+class Htb:  # htb.py:64-86
+    off: np.ndarray
+    idx: np.ndarray
+    val: np.ndarray
+
+    @property
+    def n_sets(self) -> int:
+        return len(self.off) - 1
+
+    @property
+    def n_words(self) -> int:
+        return len(self.idx)
+
+
+@dataclass
+class SearchStructures:  # engine.py:82-92, exported from device
+    choice: AnchorChoice
+    work: BipartiteGraph
+    und_sizes: np.ndarray
+    order: PriorityOrder
+    dir2: TwoHopIndex
+    adj_htb: Htb
+    dir2_htb: Htb
+    tasks: np.ndarray  # int32[(emitted, 2)] in emission order (engine.py:147-173)
+
+
+def _csr_arrays(g):
+    u, v = as_csr(g)
+    arrs = [np.ascontiguousarray(u.off, np.int64), np.ascontiguousarray(u.idx, np.int32),
+            np.ascontiguousarray(v.off, np.int64), np.ascontiguousarray(v.idx, np.int32)]
+    return arrs, u.n, v.n
+
+
+def _make_config(cfg: EngineConfig, anchor: str, rank, roots, shard=(0, 1), flags=0):
+    c = _abi.BcConfig()
+    c.batch_words = int(cfg.batch_buffer_capacity)
+    c.mode = 0 if cfg.mode == "dfs" else 1
+    c.anchor = {"auto": -1, "U": 0, "V": 1}[anchor]
+    c.order_mode = ORDER_MODES.index(cfg.order_mode)
+    c.device = int(cfg.device)
+    c.shard_index, c.shard_count = int(shard[0]), int(shard[1])
+    c.flags = flags | (_abi.BC_FLAG_INSTRUMENT if cfg.instrument else 0)
+    keep = []
+    if rank is not None:
+        r = np.ascontiguousarray(rank, dtype=np.int64)
+        keep.append(r)
+        c.rank_override = r.ctypes.data
+        c.n_rank = len(r)
+    if roots is not None:
+        rr = np.fromiter((int(x) for x in roots), dtype=np.int64)
+        rr = rr[(rr >= -(2**31)) & (rr < 2**31)].astype(np.int32)
+        keep.append(rr)
+        c.roots = rr.ctypes.data if len(rr) else keep_empty(keep)
+        c.n_roots = len(rr)
+    return c, keep
+
+
+def keep_empty(keep):
+    z = np.zeros(1, dtype=np.int32)
+    keep.append(z)
+    return z.ctypes.data
+
+
+class DeviceGraph:
+    """A graph resident in HBM (``bc_graph``): upload once, count many times."""
+
+    def __init__(self, g, device: int = 0):
+        L = _abi.load()
+        (uo, ui, vo, vi), nu, nv = _csr_arrays(g)
+        h = C.c_void_p()
+        _abi.check(L.bc_graph_create(uo.ctypes.data, ui.ctypes.data, nu, vo.ctypes.data,
+                                     vi.ctypes.data, nv, device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.u_count, self.v_count = nu, nv
+
+    def count_raw(self, p: int, q: int, cfg: EngineConfig | None = None, *, anchor=None,
+                  rank=None, roots=None, shard=(0, 1), task_counts: bool = False):
+        """One counting pass; returns (BcReport, per-task counts or None)."""
+        cfg = cfg if cfg is not None else EngineConfig()
+        cfg.validate()
+        if p < 1 or q < 1:
+            raise ValueError("p and q must be >= 1")
+        L = _abi.load()
+        flags = _abi.BC_FLAG_TASK_COUNTS if task_counts else 0
+        c, keep = _make_config(cfg, anchor or cfg.anchor, rank, roots, shard, flags)
+        tc = None
+        if task_counts:
+            # the emitted count is only known on device: size by directed pairs bound
+            cap = max(1, _task_bound(self, p, q, cfg, anchor, rank))
+            tc = np.zeros(2 * cap, dtype=np.uint64)
+            c.task_counts = tc.ctypes.data
+            c.task_counts_cap = cap
+        rep = _abi.BcReport()
+        _abi.check(L.bc_graph_count(self._h, int(p), int(q), C.byref(c), C.byref(rep)))
+        del keep
+        per_task = None
+        if task_counts:
+            e = rep.tasks_emitted
+            lo = tc[0:2 * e:2].astype(object)
+            hi = tc[1:2 * e:2].astype(object)
+            per_task = [int(a) | (int(b) << 64) for a, b in zip(lo, hi)]
+        return rep, per_task
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _abi.load().bc_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _task_bound(dg: DeviceGraph, p, q, cfg, anchor, rank) -> int:
+    s = _prepare_device(dg, p, q, cfg, anchor or cfg.anchor, rank)
+    try:
+        return int(_export(s, _abi.BC_X_TASKS).size // 2)
+    finally:
+        _abi.load().bc_structs_destroy(s)
+
+
+def _prepare_device(dg: DeviceGraph, p, q, cfg, anchor, rank, roots=None):
+    L = _abi.load()
+    c, keep = _make_config(cfg, anchor, rank, roots)
+    h = C.c_void_p()
+    _abi.check(L.bc_prepare(dg._h, int(p), int(q), C.byref(c), C.byref(h)))
+    del keep
+    return h
+
+
+_EXPORT_DT = {
+    _abi.BC_X_UND_SIZE: np.int64, _abi.BC_X_RANK: np.int64, _abi.BC_X_ORDER: np.int64,
+    _abi.BC_X_DIR_OFF: np.int64, _abi.BC_X_DIR_IDX: np.int32, _abi.BC_X_HADJ_OFF: np.int64,
+    _abi.BC_X_HADJ_IDX: np.uint32, _abi.BC_X_HADJ_VAL: np.uint32, _abi.BC_X_HDIR_OFF: np.int64,
+    _abi.BC_X_HDIR_IDX: np.uint32, _abi.BC_X_HDIR_VAL: np.uint32, _abi.BC_X_TASKS: np.int32,
+    _abi.BC_X_META: np.int64,
+}
+
+
+def _export(h, what: int) -> np.ndarray:
+    L = _abi.load()
+    n = L.bc_export_len(h, what)
+    out = np.empty(max(n, 0), dtype=_EXPORT_DT[what])
+    if n > 0:
+        _abi.check(L.bc_export(h, what, out.ctypes.data))
+    return out
+
+
+def prepare_structures(g, p: int, q: int, anchor: str = "auto", rank=None,
+                       device: int = 0, roots=None) -> SearchStructures:
+    """Device-built structures, exported (engine.py:115-144)."""
+    if p < 1 or q < 1:
+        raise ValueError("p and q must be >= 1")
+    if anchor not in ANCHOR_FLAGS:
+        raise ValueError(f"anchor must be one of {ANCHOR_FLAGS}")
+    dg = DeviceGraph(g, device)
+    cfg = EngineConfig(device=device)
+    h = _prepare_device(dg, p, q, cfg, anchor, rank, roots)
+    L = _abi.load()
+    try:
+        meta = _export(h, _abi.BC_X_META)
+        layer = "UV"[int(meta[0])]
+        choice = AnchorChoice(layer, int(meta[1]), int(meta[2]))
+        u, v = as_csr(g)
+        work = BipartiteGraph(u_csr=u, v_csr=v) if layer == "U" else BipartiteGraph(u_csr=v, v_csr=u)
+        dir2 = TwoHopIndex(choice.q_eff, "U",
+                           CsrView(_export(h, _abi.BC_X_DIR_OFF), _export(h, _abi.BC_X_DIR_IDX)),
+                           directed=True)
+        return SearchStructures(
+            choice=choice, work=work, und_sizes=_export(h, _abi.BC_X_UND_SIZE),
+            order=PriorityOrder(_export(h, _abi.BC_X_RANK), _export(h, _abi.BC_X_ORDER)),
+            dir2=dir2,
+            adj_htb=Htb(_export(h, _abi.BC_X_HADJ_OFF), _export(h, _abi.BC_X_HADJ_IDX),
+                        _export(h, _abi.BC_X_HADJ_VAL)),
+            dir2_htb=Htb(_export(h, _abi.BC_X_HDIR_OFF), _export(h, _abi.BC_X_HDIR_IDX),
+                         _export(h, _abi.BC_X_HDIR_VAL)),
+            tasks=_export(h, _abi.BC_X_TASKS).reshape(-1, 2))
+    finally:
+        L.bc_structs_destroy(h)
+        dg.close()
+
+
+def _report(rep: _abi.BcReport, cfg: EngineConfig, wall: float, anchor_layer: str,
+            per_task=None) -> CountReport:
+    d = rep.as_dict()
+    return CountReport(
+        count=d["count"], time_1hop=rep.time_level1, time_2hop=rep.time_enum,
+        batches_executed=rep.batches_executed, tasks_stolen=rep.tasks_stolen,
+        roots_filtered=rep.roots_filtered, wall_time=wall, tasks_emitted=rep.tasks_emitted,
+        tasks_consumed=rep.tasks_consumed, workers=cfg.worker_count, anchor_layer=anchor_layer,
+        task_counts=per_task, device=d)
+
+
+def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
+                    structures=None, roots=None) -> CountReport:
+    """Exact (p,q)-biclique count on the GPU (engine.py:419-500).
+
+    ``structures`` (ours or the reference's ``SearchStructures``) fixes the
+    anchor layer and the priority rank, as in the reference's partitioned
+    counting (partition.py:246-249); the device rebuilds the rest itself.
+    ``roots`` restricts which anchor vertices root tasks (engine.py:155-162).
+    ``wall_time`` covers the device call (preprocessing + counting).
+    """
+    cfg = cfg if cfg is not None else EngineConfig()
+    cfg.validate()
+    if p < 1 or q < 1:
+        raise ValueError("p and q must be >= 1")
+    anchor, rank, graph, pp, qq = cfg.anchor, None, g, p, q
+    if structures is not None:
+        # the reference reads s.work / s.choice / s.order only (engine.py:430-434)
+        graph = structures.work
+        anchor = "U"
+        pp, qq = structures.choice.p_eff, structures.choice.q_eff
+        rank = np.asarray(structures.order.rank, dtype=np.int64)
+    L = _abi.load()
+    (uo, ui, vo, vi), nu, nv = _csr_arrays(graph)
+    c, keep = _make_config(cfg, anchor, rank, roots)
+    rep = _abi.BcReport()
+    t0 = perf_counter()
+    _abi.check(L.bc_count(uo.ctypes.data, ui.ctypes.data, nu, vo.ctypes.data, vi.ctypes.data, nv,
+                          int(pp), int(qq), C.byref(c), C.byref(rep)))
+    wall = perf_counter() - t0
+    del keep
+    layer = structures.choice.layer if structures is not None else "UV"[rep.anchor]
+    return _report(rep, cfg, wall, layer)
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU: shard tasks across ranks, one allreduce of the 128-bit partials
+# ---------------------------------------------------------------------------
+def split_limbs(x: int) -> list[int]:
+    """128-bit count -> four 32-bit limbs (each summed in a u64 lane)."""
+    if x < 0 or x >= 1 << 128:
+        raise ValueError("partial count outside [0, 2^128)")
+    return [(x >> (32 * i)) & 0xFFFFFFFF for i in range(4)]
+
+
+def merge_limbs(limbs) -> int:
+    """Carry-normalise summed limbs (exact for up to 2^32 ranks)."""
+    return sum(int(v) << (32 * i) for i, v in enumerate(limbs))
+
+
+def allreduce_count(partial: int, group=None, device=None) -> int:
+    """Sum exact partial counts over a torch.distributed group.
+
+    One ``all_reduce(SUM)`` of 4 x int64 limbs (NCCL over NVLink on GPUs,
+    gloo on CPU); each limb holds < 2^32, so the sum is exact for < 2^31
+    ranks in a signed 64-bit lane.
+    """
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(split_limbs(partial), dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return merge_limbs(t.cpu().tolist())
+
+
+def count_bicliques_distributed(g, p: int, q: int, cfg: EngineConfig | None = None, *,
+                                rank: int, world: int, group=None, dgraph: DeviceGraph | None = None,
+                                roots=None) -> tuple[int, CountReport]:
+    """This rank counts tasks t with t % world == rank; returns (total, local report)."""
+    cfg = cfg if cfg is not None else EngineConfig()
+    dg = dgraph if dgraph is not None else DeviceGraph(g, cfg.device)
+    t0 = perf_counter()
+    rep, _ = dg.count_raw(p, q, cfg, roots=roots, shard=(rank, world))
+    wall = perf_counter() - t0
+    local = _report(rep, cfg, wall, "UV"[rep.anchor])
+    import torch
+
+    dev = torch.device("cuda", cfg.device) if torch.cuda.is_available() else None
+    total = allreduce_count(local.count, group, dev)
+    return total, local

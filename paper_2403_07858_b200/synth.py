@@ -1,0 +1,221 @@
+"""Seeded synthetic inputs: the five BASELINE.json configs and the test corpora.
+
+Recipes follow SURVEY.md Appendix B (RNG call sequences reproduced exactly
+so the sha256 fingerprints there match). Two generators restate reference
+code because the parity graphs are defined by it:
+
+* ``synth_generate`` — power-law 2-hop generator, reference
+  ``pkg/src/bicount/cli.py:58-110`` (C4's background graph).
+* ``random_bipartite`` / ``corpus300`` / ``recon_graph`` — reference test
+  fixtures ``pkg/tests/helpers.py:7-55``.
+
+All are deterministic per seed (numpy PCG64 ``default_rng``).
+"""
+
+from __future__ import annotations
+
+import warnings
+from math import comb
+
+import numpy as np
+
+from .graph import BipartiteGraph, csr_from_sorted_keys, from_edges
+
+# cli.py:34-36 synthesis knobs
+TARGET_FLOOR = 40
+SHARE_BIAS = 0.55
+STALL_LIMIT = 24
+
+FINGERPRINTS = {
+    "C1": "3ab2e3e23871d9015d46a92a21676aac8a23c3fd7aca34e13902f531c1df9117",
+    "C2": "5971ce6f3745cc286c68e95cf0fd0e5ef7244f449019e1dbd5114a696e0b2c14",
+    "C3": "7b3cfe96d091cbad4bdce0ceeeb9ef21e0cfb7db002fcc71a016c1e607ae8b2d",
+    "C4": "cf71d0fac1cc00b4a5a5749833c6de35811bd50268f90c4637ebdec3903962ed",
+}
+
+RECON_U_NEIGHBORS = [[0, 1, 2], [0, 1, 2, 4], [1, 2, 3], [0, 2, 3, 4]]
+CORPUS_SEED = 20260822
+
+
+def recon_graph() -> BipartiteGraph:
+    """The 4x5 example graph of the paper's Examples 1-3 (helpers.py:10-24)."""
+    eu = [u for u, nb in enumerate(RECON_U_NEIGHBORS) for _ in nb]
+    ev = [v for nb in RECON_U_NEIGHBORS for v in nb]
+    return from_edges(4, 5, eu, ev)
+
+
+def random_bipartite(nu: int, nv: int, density: float, seed) -> BipartiteGraph:
+    """Dense Bernoulli mask graph (helpers.py:27-31)."""
+    rng = np.random.default_rng(seed)
+    mask = rng.random((nu, nv)) < density
+    eu, ev = np.nonzero(mask)
+    return from_edges(nu, nv, eu, ev)
+
+
+def corpus300() -> list[BipartiteGraph]:
+    """300 seeded graphs <= 30+30 vertices, density 0.1-0.5 (helpers.py:37-55)."""
+    rng = np.random.default_rng(CORPUS_SEED)
+    out = []
+    while len(out) < 300:
+        nu = int(rng.integers(2, 31))
+        nv = int(rng.integers(2, 31))
+        if comb(nu, 4) * comb(nv, 4) > 10**8:
+            continue
+        density = float(rng.uniform(0.1, 0.5))
+        out.append(random_bipartite(nu, nv, density, rng.integers(0, 2**31)))
+    return out
+
+
+def synth_generate(u_count: int, v_count: int, alpha: float, seed: int) -> BipartiteGraph:
+    """Power-law 2-hop generator (reference cli.py:58-110).
+
+    Each U vertex draws a 2-hop target from a truncated power law and adds
+    V neighbours (biased towards popular ones) until the target is met or
+    the pick loop stalls. The draw order of ``rng`` is part of the contract.
+    """
+    if u_count < 1 or v_count < 1:
+        raise ValueError("layer sizes must be >= 1")
+    if alpha <= 1:
+        raise ValueError("power-law exponent must be > 1")
+    rng = np.random.default_rng(seed)
+    cap = max(1, u_count - 1)
+    raw = np.floor(TARGET_FLOOR * (1.0 - rng.random(u_count))
+                   ** (-1.0 / (alpha - 1.0))).astype(np.int64)
+    if int((raw > cap).sum()):
+        warnings.warn(f"{int((raw > cap).sum())} of {u_count} two-hop targets "
+                      f"exceed {cap} and were clipped", RuntimeWarning)
+    targets = np.minimum(raw, cap).tolist()
+    holders: list[list[int]] = [[] for _ in range(v_count)]
+    picks: list[int] = []
+    eu: list[int] = []
+    ev: list[int] = []
+    for u in range(u_count):
+        goal = targets[u]
+        seen: set[int] = set()
+        mine: set[int] = set()
+        misses = 0
+        while len(seen) < goal and misses < STALL_LIMIT and len(mine) < v_count:
+            if picks and rng.random() < SHARE_BIAS:
+                v = picks[int(rng.integers(len(picks)))]
+            else:
+                v = int(rng.integers(v_count))
+            if v in mine:
+                misses += 1
+                continue
+            had = len(seen)
+            mine.add(v)
+            seen.update(holders[v])
+            holders[v].append(u)
+            picks.append(v)
+            misses = 0 if len(seen) > had else misses + 1
+        for v in sorted(mine):
+            eu.append(u)
+            ev.append(v)
+    return from_edges(u_count, v_count, eu, ev)
+
+
+def erdos_renyi(nu: int, nv: int, m: int, seed: int) -> BipartiteGraph:
+    rng = np.random.default_rng(seed)
+    keys = rng.choice(nu * nv, size=m, replace=False)
+    return from_edges(nu, nv, keys // nv, keys % nv)
+
+
+def chung_lu(nu: int, nv: int, m: int, gamma: float, seed: int, over: float) -> BipartiteGraph:
+    """Chung-Lu power-law bipartite graph (SURVEY App. B recipe)."""
+    rng = np.random.default_rng(seed)
+
+    def w(n):
+        x = (np.arange(n) + 1.0) ** (-1.0 / (gamma - 1.0))
+        return x / x.sum()
+
+    k = int(m * over)
+    eu = rng.choice(nu, k, p=w(nu))
+    ev = rng.choice(nv, k, p=w(nv))
+    key = np.unique(eu.astype(np.int64) * nv + ev)
+    key = rng.permutation(key)[:m]
+    return from_edges(nu, nv, key // nv, key % nv)
+
+
+PLANTED_CORES = [(32, 48, 0.85), (24, 32, 0.9), (20, 24, 0.95)]
+
+
+def planted_dense(seed_base: int = 7, seed_cores: int = 3) -> BipartiteGraph:
+    """C4: S2-shaped synth + 3 planted dense cores."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        base = synth_generate(12720, 11100, 2.6, seed_base)
+    rng = np.random.default_rng(seed_cores)
+    eu = [np.repeat(np.arange(base.u_count, dtype=np.int64), base.u_csr.degrees())]
+    ev = [base.u_csr.idx.astype(np.int64)]
+    for a, b, dens in PLANTED_CORES:
+        cu = rng.choice(12720, a, replace=False)
+        cv = rng.choice(11100, b, replace=False)
+        mask = rng.random((a, b)) < dens
+        i, j = np.nonzero(mask)
+        eu.append(cu[i].astype(np.int64))
+        ev.append(cv[j].astype(np.int64))
+    return from_edges(12720, 11100, np.concatenate(eu), np.concatenate(ev))
+
+
+def fr_shaped(nu: int = 44_000, nv: int = 8_956_000, m: int = 100_000_000,
+              gamma_u: float = 2.5, gamma_v: float = 2.5, cap_u: float = 200_000,
+              cap_v: float = 64, seed: int = 5, n_cores: int = 64,
+              core_seed: int = 9) -> BipartiteGraph:
+    """C5: FR-shaped capped Chung-Lu + planted dense cores.
+
+    Small dense U, huge sparse V (|V|/|U| ~ 202). Expected degrees are
+    iteratively clipped at cap/m; endpoints sampled by inverse CDF; then
+    ``n_cores`` copies of C4's three core shapes are planted at random
+    positions so the (8,8) count is non-trivial.
+    """
+    rng = np.random.default_rng(seed)
+
+    def capped(n, gamma, cap):
+        w = (np.arange(n) + 1.0) ** (-1.0 / (gamma - 1.0))
+        w /= w.sum()
+        lim = cap / m
+        for _ in range(30):
+            w = np.minimum(w, lim)
+            w /= w.sum()
+        return np.cumsum(w)
+
+    k = int(m * 1.15)
+    cu = capped(nu, gamma_u, cap_u)
+    eu = np.searchsorted(cu, rng.random(k) * cu[-1], side="right").astype(np.int64)
+    np.minimum(eu, nu - 1, out=eu)
+    del cu
+    cv = capped(nv, gamma_v, cap_v)
+    ev = np.searchsorted(cv, rng.random(k) * cv[-1], side="right").astype(np.int64)
+    np.minimum(ev, nv - 1, out=ev)
+    del cv
+    key = eu * nv + ev
+    del eu, ev
+    key = np.unique(key)
+    if len(key) > m:
+        key = rng.permutation(key)[:m]
+    crng = np.random.default_rng(core_seed)
+    extra = []
+    for _ in range(n_cores):
+        for a, b, dens in PLANTED_CORES:
+            pu = crng.choice(nu, a, replace=False).astype(np.int64)
+            pv = crng.choice(nv, b, replace=False).astype(np.int64)
+            i, j = np.nonzero(crng.random((a, b)) < dens)
+            extra.append(pu[i] * nv + pv[j])
+    if extra:
+        key = np.concatenate([key] + extra)
+    key = np.unique(key)
+    return csr_from_sorted_keys(nu, nv, key)
+
+
+CONFIGS = {
+    # name: (builder, [(p, q), ...])
+    "C1": (lambda: erdos_renyi(2000, 2000, 20000, 1), [(2, 2)]),
+    "C2": (lambda: chung_lu(100000, 50000, 1000000, 2.5, 7, 1.15), [(4, 4)]),
+    "C3": (lambda: chung_lu(56519, 120867, 440237, 2.5, 11, 1.3), [(3, 6), (6, 3)]),
+    "C4": (planted_dense, [(8, 8)]),
+    "C5": (fr_shaped, [(8, 8)]),
+}
+
+
+def build_config(name: str) -> BipartiteGraph:
+    return CONFIGS[name][0]()

@@ -1,0 +1,101 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/bicount_b200.h declares, ctypes layouts match the header,
+and the product path refuses to run without a device (no CPU fallback)."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2403_07858_b200 import _abi, build
+from paper_2403_07858_b200.engine import EngineConfig, merge_limbs, split_limbs
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "bicount_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _abi.open_library()
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(bc_\w+)\s*\(", text, re.M)))
+
+
+def test_exports_every_declared_symbol(lib):
+    declared = header_functions()
+    assert set(declared) == set(_abi.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_abi_version_and_device_probe(lib):
+    assert lib.bc_abi_version() == 1
+    assert lib.bc_device_count() >= 0
+
+
+def test_struct_layout_matches_header():
+    # bc_config: 8 x int32, then ptr/int64 pairs x 3 -> 32 + 48 = 80 bytes
+    assert C.sizeof(_abi.BcConfig) == 80
+    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 = 16 + 16 + 144 + 40
+    assert C.sizeof(_abi.BcReport) == 216
+    text = open(HEADER).read()
+    cfg_body = re.search(r"typedef struct bc_config \{(.*?)\} bc_config;", text, re.S).group(1)
+    names = re.findall(r"\*?(\w+)\s*(?:,|;)", re.sub(r"/\*.*?\*/", "", cfg_body, flags=re.S))
+    assert [f for f, _ in _abi.BcConfig._fields_] == names
+    rep_body = re.search(r"typedef struct bc_report \{(.*?)\} bc_report;", text, re.S).group(1)
+    rep_names = re.findall(r"(\w+)\s*(?:,|;)", re.sub(r"/\*.*?\*/", "", rep_body, flags=re.S))
+    assert [f for f, _ in _abi.BcReport._fields_] == rep_names
+
+
+@pytest.mark.skipif(_abi.open_library().bc_device_count() > 0 if os.path.exists(_abi.LIB_PATH) else False,
+                    reason="a GPU is present")
+def test_no_cpu_fallback_without_device(lib):
+    from paper_2403_07858_b200 import count_bicliques, synth
+
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        count_bicliques(synth.recon_graph(), 3, 2)
+
+
+def test_invalid_arguments_fail_before_device(lib):
+    from paper_2403_07858_b200 import count_bicliques, synth
+
+    g = synth.recon_graph()
+    with pytest.raises(ValueError):
+        count_bicliques(g, 3, 2, EngineConfig(worker_count=0))
+    with pytest.raises(ValueError):
+        count_bicliques(g, 3, 2, EngineConfig(mode="bfs"))
+    with pytest.raises(ValueError):
+        count_bicliques(g, 3, 2, EngineConfig(anchor="W"))
+    with pytest.raises(ValueError):
+        count_bicliques(g, 0, 2)
+    with pytest.raises(NotImplementedError):
+        count_bicliques(g, 3, 2, EngineConfig(enumerate_results=True))
+
+
+@pytest.mark.parametrize("x", [0, 1, 2**32 - 1, 2**32, 2**64 + 5, 2**128 - 1, 90068795717])
+def test_limbs_roundtrip(x):
+    assert merge_limbs(split_limbs(x)) == x
+    # summing limbs of several partials then normalising equals the exact sum
+    parts = [x, (x * 7 + 3) % 2**126, 12345]
+    summed = [sum(col) for col in zip(*(split_limbs(v) for v in parts))]
+    assert merge_limbs(summed) == sum(parts)
+
+
+def test_graph_csr_matches_reference_shape():
+    from paper_2403_07858_b200 import synth
+
+    g = synth.recon_graph()
+    assert [a.tolist() for a in g.u_adj] == synth.RECON_U_NEIGHBORS
+    assert g.edge_count == 14
+    t = synth.transpose(g) if hasattr(synth, "transpose") else None
+    from paper_2403_07858_b200.graph import transpose
+
+    t = transpose(g)
+    assert t.u_count == 5 and t.v_count == 4
+    assert np.array_equal(t.u_csr.idx, g.v_csr.idx)
