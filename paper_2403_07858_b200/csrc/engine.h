@@ -86,6 +86,12 @@ struct DevStructs {
   DBuf<int64_t> hadj_off, hdir_off;
   DBuf<uint32_t> hadj_idx, hadj_val, hdir_idx, hdir_val;
   DBuf<int2> tasks;  // (root, second) in emission order
+  // dense bitmaps of the longest adjacency rows (hubs): dense[slot * dense_mw + w] is the
+  // HTB Val of word w (0 if absent); dense_id[x] = slot or -1
+  DBuf<int32_t> dense_id;
+  DBuf<uint32_t> dense;
+  int64_t dense_mw = 0, dense_rows = 0;
+  int dense_T = 0;
   int64_t emitted = 0, filtered = 0;
   int64_t und_pairs = 0, dir2_pairs = 0, adj_words = 0, dir2_words = 0;
   int64_t max_adj_slice = 0, max_dir_slice = 0;

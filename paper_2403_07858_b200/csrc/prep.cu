@@ -37,11 +37,15 @@ T d2h_scalar(const T *p, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // 2-hop index: one CTA per anchor vertex u (dynamic queue, heaviest first).
 // Counters for ids of the current tile live in shared memory (two u16 per
-// u32 word, or one u32 per id when WIDE).  Increments stop once a counter
-// reaches k (the reads are racy but monotone, so a stale read only costs one
-// extra increment; at most blockDim extra increments per id keep u16 safe).
-// The kept ids (count >= k, != u) are emitted in ascending order by scanning
-// the counter tile, which also zeroes it for the next vertex.
+// u32 word, or one u32 per id when WIDE), next to a "touched" bitmap with one
+// bit per id.  Increments stop once a counter reaches k (the reads are racy
+// but monotone: a stale read costs one extra increment, at most blockDim per
+// id, which keeps u16 counters exact below k <= 60000).  The first increment
+// of an id sets its touched bit, so the emit phase visits only the touched
+// 32-id words: pass 1 turns each touched word into its kept mask (count >= k,
+// id != u) and clears the counters; pass 2 writes the kept ids in ascending
+// order with a block-wide exclusive scan and clears the bitmap.  Cost per
+// vertex is O(pool + n/32), not O(n).
 // ---------------------------------------------------------------------------
 constexpr int TH_THREADS = 512;
 
@@ -59,14 +63,22 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
     int *next, int64_t *__restrict__ und_size, int64_t *__restrict__ seg_start,
     int32_t *__restrict__ seg_len, int32_t *__restrict__ out_ids, int64_t out_cap,
     unsigned long long *out_used, int *overflow) {
-  extern __shared__ uint32_t ctr[];
-  __shared__ int64_t s_u;
-  __shared__ int s_warp[TH_THREADS / 32];
-  __shared__ int64_t s_base;
+  typedef cub::BlockScan<int, TH_THREADS> Scan;
+  typedef cub::BlockReduce<int, TH_THREADS> Reduce;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Reduce::TempStorage reduce;
+  } tmp;
+  extern __shared__ uint32_t sm[];
+  const int64_t nctr = WIDE ? tile : (tile + 1) / 2;
+  const int64_t nbits = (tile + 31) / 32;
+  uint32_t *ctr = sm;
+  uint32_t *touched = sm + nctr;
+  __shared__ int64_t s_u, s_base;
+  __shared__ int s_total;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = TH_THREADS / 32;
-  const int64_t nwords = WIDE ? tile : (tile + 1) / 2;
-  for (int64_t i = tid; i < nwords; i += TH_THREADS) ctr[i] = 0;
+  for (int64_t i = tid; i < nctr + nbits; i += TH_THREADS) sm[i] = 0;
   __syncthreads();
   for (;;) {
     if (tid == 0) {
@@ -89,27 +101,48 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
           const int64_t w = __ldg(bidx + f);
           if (w < t0 || w >= t1) continue;
           const int64_t l = w - t0;
+          bool first;
           if (WIDE) {
-            if (((volatile uint32_t *)ctr)[l] < k) atomicAdd(&ctr[l], 1u);
+            if (((volatile uint32_t *)ctr)[l] >= k) continue;
+            first = atomicAdd(&ctr[l], 1u) == 0;
           } else {
             const int sh = (int)(l & 1) * 16;
-            uint32_t c = (((volatile uint32_t *)ctr)[l >> 1] >> sh) & 0xffffu;
-            if (c < k) atomicAdd(&ctr[l >> 1], 1u << sh);
+            if (((((volatile uint32_t *)ctr)[l >> 1] >> sh) & 0xffffu) >= k) continue;
+            first = ((atomicAdd(&ctr[l >> 1], 1u << sh) >> sh) & 0xffffu) == 0;
           }
+          if (first) atomicOr(&touched[l >> 5], 1u << (l & 31));
         }
       }
       __syncthreads();
-      // kept-count phase
-      const int64_t len = t1 - t0;
+      // pass 1: touched words -> kept masks, counters cleared
+      const int64_t nt = (t1 - t0 + 31) / 32;
       int mine = 0;
-      for (int64_t l = tid; l < len; l += TH_THREADS)
-        mine += (ctr_get<WIDE>(ctr, l) >= k && t0 + l != u) ? 1 : 0;
-      mine = __reduce_add_sync(FULL, mine);
-      if (lane == 0) s_warp[warp] = mine;
-      __syncthreads();
+      for (int64_t wi = tid; wi < nt; wi += TH_THREADS) {
+        uint32_t t = touched[wi], km = 0;
+        if (!t) continue;
+        uint32_t m = t;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          const int64_t l = wi * 32 + b;
+          if (ctr_get<WIDE>(ctr, l) >= k && t0 + l != u) km |= 1u << b;
+        }
+        if (WIDE) {
+          m = t;
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            ctr[wi * 32 + b] = 0;
+          }
+        } else {
+          for (int h = 0; h < 16; h++)
+            if ((t >> (2 * h)) & 3u) ctr[wi * 16 + h] = 0;
+        }
+        touched[wi] = km;
+        mine += __popc(km);
+      }
+      const int kept = Reduce(tmp.reduce).Sum(mine);
       if (tid == 0) {
-        int64_t kept = 0;
-        for (int w = 0; w < nwarps; w++) kept += s_warp[w];
         int64_t base = -1;
         if (kept) {
           unsigned long long b = atomicAdd(out_used, (unsigned long long)kept);
@@ -117,34 +150,36 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
           else base = (int64_t)b;
         }
         s_base = base;
+        s_total = kept;
         seg_start[u * ntiles + ti] = base;
-        seg_len[u * ntiles + ti] = (int32_t)kept;
-        s_warp[0] = (int)kept;
+        seg_len[u * ntiles + ti] = kept;
       }
       __syncthreads();
-      total += s_warp[0];
+      total += s_total;
       const int64_t base = s_base;
-      __syncthreads();
-      // write phase (ascending ids, order-preserving) + zero the tile
+      // pass 2: ordered emit of the kept ids, bitmap cleared
       int64_t pos = 0;
-      for (int64_t c0 = 0; c0 < len; c0 += TH_THREADS) {
-        const int64_t l = c0 + tid;
-        bool keep = false;
-        if (l < len) keep = ctr_get<WIDE>(ctr, l) >= k && t0 + l != u;
-        const unsigned b = __ballot_sync(FULL, keep);
-        if (lane == 0) s_warp[warp] = __popc(b);
-        __syncthreads();
-        int before = 0, all = 0;
-        for (int w = 0; w < nwarps; w++) {
-          int c = s_warp[w];
-          before += (w < warp) ? c : 0;
-          all += c;
+      if (s_total) {
+        for (int64_t r0 = 0; r0 < nt; r0 += TH_THREADS) {
+          const int64_t wi = r0 + tid;
+          uint32_t km = wi < nt ? touched[wi] : 0u;
+          int off, round;
+          Scan(tmp.scan).ExclusiveSum(__popc(km), off, round);
+          if (km) {
+            touched[wi] = 0;
+            if (base >= 0) {
+              int64_t o = base + pos + off;
+              while (km) {
+                const int b = __ffs(km) - 1;
+                km &= km - 1;
+                out_ids[o++] = (int32_t)(t0 + wi * 32 + b);
+              }
+            }
+          }
+          pos += round;
+          __syncthreads();
         }
-        if (keep && base >= 0) out_ids[base + pos + before + __popc(b & lanemask_lt())] = (int32_t)(t0 + l);
-        pos += all;
-        __syncthreads();
       }
-      for (int64_t i = tid; i < (WIDE ? len : (len + 1) / 2); i += TH_THREADS) ctr[i] = 0;
       __syncthreads();
     }
     if (tid == 0) und_size[u] = total;
@@ -259,6 +294,41 @@ __global__ void htb_build(const int64_t *__restrict__ off, const int32_t *__rest
       pos += __popc(m);
     }
     if (!WRITE && lane == 0) words[u] = pos - (WRITE ? hoff[u] : 0);
+  }
+}
+
+// dense hub rows: histogram of rows with more than 16 << i words
+constexpr int DENSE_NT = 12;
+__global__ void dense_hist(const int64_t *hoff, int64_t n, unsigned long long *hist) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t w = hoff[i + 1] - hoff[i];
+  for (int t = 0; t < DENSE_NT; t++)
+    if (w > (int64_t(16) << t)) atomicAdd(hist + t, 1ull);
+}
+
+__global__ void dense_flags(const int64_t *hoff, int64_t n, int64_t T, int32_t *flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = (hoff[i + 1] - hoff[i]) > T ? 1 : 0;
+}
+
+__global__ void dense_ids(const int32_t *flag, const int32_t *slot, int64_t n, int32_t *id) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) id[i] = flag[i] ? slot[i] : -1;
+}
+
+__global__ void dense_fill(const int64_t *__restrict__ hoff, const uint32_t *__restrict__ hidx,
+                           const uint32_t *__restrict__ hval, int64_t n,
+                           const int32_t *__restrict__ id, uint32_t *__restrict__ dense,
+                           int64_t mw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = gw; x < n; x += nw) {
+    const int32_t sl = id[x];
+    if (sl < 0) continue;
+    uint32_t *row = dense + (int64_t)sl * mw;
+    for (int64_t j = hoff[x] + lane; j < hoff[x + 1]; j += 32) row[hidx[j]] = hval[j];
   }
 }
 
@@ -399,12 +469,14 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
   if (n > 0 && (int64_t)k <= s.max_deg_anchor) {
     int smem_optin = 0;
     BC_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g.device));
-    const int64_t max_words = (smem_optin - 4096) / 4;
-    const int64_t max_tile = wide ? max_words : 2 * max_words;
+    // counters + touched bitmap per tile id: 2 B + 1/8 B (u16) or 4 B + 1/8 B (u32)
+    const int64_t budget_bits = (int64_t)(smem_optin - 8192) * 8;
+    int64_t max_tile = wide ? budget_bits / 33 : budget_bits / 17;
+    max_tile &= ~int64_t(63);
     ntiles = (int)((n + max_tile - 1) / max_tile);
     tile = (n + ntiles - 1) / ntiles;
-    if (!wide) tile = (tile + 1) & ~int64_t(1);
-    const size_t smem = (size_t)(wide ? tile : tile / 2) * 4;
+    tile = (tile + 63) & ~int64_t(63);
+    const size_t smem = (size_t)((wide ? tile : (tile + 1) / 2) + (tile + 31) / 32) * 4;
     auto kern = wide ? twohop_kernel<true> : twohop_kernel<false>;
     BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -524,6 +596,47 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
             sms, st, L);
   build_htb(s.dir_off.p, s.dir_idx.p, n, s.hdir_off, s.hdir_idx, s.hdir_val, s.dir2_words,
             s.max_dir_slice, sms, st, L);
+
+  // ---- dense bitmaps of the longest adjacency rows (probe = one load) ----
+  s.dense_id.alloc(n ? n : 1, st);
+  BC_CUDA(cudaMemsetAsync(s.dense_id.p, 0xff, (n ? n : 1) * sizeof(int32_t), st));
+  s.dense_mw = (s.m + 31) / 32;
+  if (n > 0 && s.m > 0) {
+    DBuf<unsigned long long> hist;
+    hist.alloc(DENSE_NT, st);
+    hist.zero();
+    dense_hist<<<blocks_for(n, 256), 256, 0, st>>>(s.hadj_off.p, n, hist.p);
+    unsigned long long h[DENSE_NT];
+    copy_d2h(h, hist.p, sizeof h, st);
+    BC_CUDA(cudaStreamSynchronize(st));
+    const int64_t budget = int64_t(64) << 20;  // bytes of dense rows (stays L2-resident)
+    int pick = -1;
+    for (int t = 0; t < DENSE_NT; t++) {
+      const int64_t T = int64_t(16) << t;
+      if (T >= s.dense_mw / 4) break;  // a row that long is already dense-ish: no gain
+      if (h[t] > 0 && (int64_t)h[t] * s.dense_mw * 4 <= budget) {
+        pick = t;
+        break;
+      }
+    }
+    L += 1;
+    if (pick >= 0) {
+      s.dense_T = 16 << pick;
+      s.dense_rows = (int64_t)h[pick];
+      DBuf<int32_t> flag, slot;
+      flag.alloc(n, st);
+      slot.alloc(n, st);
+      dense_flags<<<blocks_for(n, 256), 256, 0, st>>>(s.hadj_off.p, n, s.dense_T, flag.p);
+      exclusive_scan(flag.p, slot.p, n, st);
+      dense_ids<<<blocks_for(n, 256), 256, 0, st>>>(flag.p, slot.p, n, s.dense_id.p);
+      s.dense.alloc((size_t)s.dense_rows * s.dense_mw, st);
+      s.dense.zero();
+      dense_fill<<<warp_blocks(n, sms), 256, 0, st>>>(s.hadj_off.p, s.hadj_idx.p, s.hadj_val.p, n,
+                                                      s.dense_id.p, s.dense.p, s.dense_mw);
+      BC_CHECK_LAUNCH();
+      L += 4;
+    }
+  }
 
   // ---- tasks (engine.py:147-173) ----
   {

@@ -4,27 +4,34 @@
 // and the leaf rule C(|C_R|, q) (engine.py:285, 346-347), for all tasks of
 // this shard, with exact 128-bit counts.
 //
-// Level 1 (kernel level1_kernel, warp per task): C_R1 = adj[r] & adj[s] and,
-// when p_eff >= 3 and |C_R1| >= q, C_L1 = dir2[r] & dir2[s] -- the same two
-// HTB intersections the reference performs first (engine.py:277-292), as a
-// warp-cooperative walk of the shorter Idx run with per-lane lower_bound in the
-// longer one (the reference's bisect, htb.py:122-154, 32 words at a time),
-// AND of the matched Val words and __popc / __reduce_add_sync reductions.
-// p_eff = 2 finishes here.  For deeper searches it records |C_R1|, |C_L1|
-// and their HTB word counts, drops tasks failing prune_keep (engine.py:110-112)
-// and emits a cost key |C_L1|*|C_R1| for the pre-runtime LPT order.
+// Level 1 (level1_kernel, warp per task): C_R1 = adj[r] & adj[s] and, when
+// p_eff >= 3 and |C_R1| >= q, C_L1 = dir2[r] & dir2[s] -- the same two HTB
+// intersections the reference performs first (engine.py:277-292).  The warp
+// walks the shorter Idx run 32 words at a time; each lane finds its word in
+// the longer run by lower_bound (the reference's bisect, htb.py:122-154) or,
+// when the longer row is a hub with a dense bitmap, by one direct load; the
+// matched Val words are ANDed and reduced with __popc / __reduce_add_sync.
+// p_eff = 2 finishes here.  Deeper searches record |C_R1|, |C_L1| and their
+// HTB word counts, drop tasks failing prune_keep (engine.py:110-112) and emit
+// the cost key |C_L1|*|C_R1| for the pre-runtime LPT order.
 //
-// Enumeration (kernel enum_kernel): persistent warps pull tasks, heaviest
-// first, from one global atomic cursor (runtime stealing).  Every deeper
-// C_R is a subset of C_R1 and every deeper C_L a subset of C_L1
-// (engine.py:296-297, 365-366), so the warp re-materialises C_R1 / C_L1 as
-// HTB words in shared memory and re-indexes them as a task-local universe:
+// Enumeration (enum_kernel): persistent warps pull tasks, heaviest first,
+// from one global atomic cursor (runtime stealing).  Every deeper C_R is a
+// subset of C_R1 and every deeper C_L a subset of C_L1 (engine.py:296-297,
+// 365-366), so the warp re-materialises C_R1 / C_L1 as HTB words and
+// re-indexes them as a task-local universe:
 //   rowR[x] = N(x) & C_R1,   rowL[x] = dir2(x) & C_L1   for x in C_L1,
 // dense bitsets over the local indices (the reference's level 1->2
 // intersections, engine.py:338, 360).  Every deeper intersection is then an
 // aligned AND of ceil(|C_R1|/32) resp. ceil(|C_L1|/32) words + popcount.
 // A node's candidates are expanded as one BFS batch across the 32 lanes and
 // the search descends depth-first into survivors (hybrid DFS-BFS, Alg. 1).
+//
+// Heavy tasks (the head of the LPT queue, p_eff >= 5) are split: their frame
+// goes to a global arena and the nodes of the split level are pushed to a
+// sub-task array that sub_kernel drains with every warp (composite balancing:
+// pre-runtime LPT order + runtime stealing + intra-task splitting).
+//
 // The reference's batch accounting (engine.py:306-331) is reproduced exactly:
 // a node's C_R / C_L word counts in the original id space are the number of
 // C_R1 / C_L1 HTB words its local bitset touches.
@@ -39,13 +46,16 @@ namespace bc {
 
 namespace {
 
-struct Graph2 {  // HTB arenas (htb.py:64-86)
+struct Graph2 {  // HTB arenas (htb.py:64-86) + dense hub rows
   const int64_t *__restrict__ aoff;
   const uint32_t *__restrict__ aidx;
   const uint32_t *__restrict__ aval;
   const int64_t *__restrict__ doff;
   const uint32_t *__restrict__ didx;
   const uint32_t *__restrict__ dval;
+  const int32_t *__restrict__ dense_id;
+  const uint32_t *__restrict__ dense;
+  int64_t mw;
 };
 
 struct Params {
@@ -62,14 +72,34 @@ struct Params {
   int *overflow;
   unsigned long long *ctr;              // counters, see CTR_*
   unsigned long long *task_counts;      // optional [2 * n_tasks]
+  int map_words;                        // anchor-word slot map entries (0 = no map)
 };
 
-enum { CTR_ALIVE = 0, CTR_BATCHES, CTR_STOLEN, CTR_INTER, CTR_OPW, CTR_MINW, CTR_MAXNEED,
-       CTR_SPILL, CTR_NEXT, CTR_COUNT };
+enum { CTR_ALIVE = 0, CTR_BATCHES, CTR_STOLEN, CTR_INTER, CTR_OPW, CTR_MINW, CTR_MAXRO,
+       CTR_MAXSCR, CTR_SPILL, CTR_NEXT, CTR_SUB_USED, CTR_SUB_N, CTR_SUB_NEXT, CTR_SPLIT,
+       CTR_COUNT };
 
 struct Info {  // level-1 facts of one task
   int32_t cr, wr, cl, wl;
 };
+
+struct Dims {
+  int nR, nL, wR, wL, WR, WL;
+  bool r_single, l_single;  // every C_R1 / C_L1 HTB word holds exactly one id
+};
+
+__device__ __forceinline__ Dims dims_of(const Info &in) {
+  Dims d;
+  d.nR = in.cr;
+  d.nL = in.cl;
+  d.wR = in.wr;
+  d.wL = in.wl;
+  d.WR = (in.cr + 31) >> 5;
+  d.WL = (in.cl + 31) >> 5;
+  d.r_single = in.wr == in.cr;
+  d.l_single = in.wl == in.cl;
+  return d;
+}
 
 __device__ __forceinline__ void add_comb(const Params &P, Acc128 &a, int c) {
   if (c >= P.first_bad) {
@@ -80,49 +110,19 @@ __device__ __forceinline__ void add_comb(const Params &P, Acc128 &a, int c) {
   a.add(v.x, v.y);
 }
 
-// Warp-cooperative HTB intersection (htb.py:122-154) returning |A&B| and the
-// number of nonzero result words.  Slices [a0,a1), [b0,b1) of one arena.
-__device__ __forceinline__ void warp_isect_count(const uint32_t *__restrict__ idx,
-                                                 const uint32_t *__restrict__ val, int64_t a0,
-                                                 int64_t a1, int64_t b0, int64_t b1, int &card,
-                                                 int &words) {
+// Warp-cooperative HTB intersection of slices [a0,a1) and [b0,b1) of one arena
+// (htb.py:122-154).  Walks the shorter slice 32 words at a time.  Matches in
+// the longer slice come from `dense_b` (its dense bitmap row) when given, else
+// from a per-lane lower_bound with a moving lower bound.  Returns |A & B| in
+// card and the number of nonzero words; with OUT, writes the nonzero words
+// (ascending) and exclusive prefix popcounts (o_pre[words] = card).
+template <bool OUT>
+__device__ __forceinline__ int warp_isect(const uint32_t *__restrict__ idx,
+                                          const uint32_t *__restrict__ val, int64_t a0,
+                                          int64_t a1, int64_t b0, int64_t b1,
+                                          const uint32_t *__restrict__ dense_b, int &card,
+                                          uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
   const int lane = lane_id();
-  if (a1 - a0 > b1 - b0) {
-    int64_t t0 = a0, t1 = a1;
-    a0 = b0; a1 = b1; b0 = t0; b1 = t1;
-  }
-  int c = 0, w = 0;
-  int64_t lo = b0;
-  for (int64_t base = a0; base < a1; base += 32) {
-    const int64_t i = base + lane;
-    int64_t j = b1;
-    uint32_t x = 0;
-    if (i < a1) {
-      const uint32_t key = __ldg(idx + i);
-      j = lower_bound_u32(idx, lo, b1, key);
-      if (j < b1 && __ldg(idx + j) == key) x = __ldg(val + i) & __ldg(val + j);
-    }
-    c += __popc(x);
-    w += x != 0;
-    const int64_t jl = __shfl_sync(FULL, j, 31);
-    if (jl >= b1) break;
-    lo = jl;
-  }
-  card = __reduce_add_sync(FULL, c);
-  words = __reduce_add_sync(FULL, w);
-}
-
-// Same walk, writing the nonzero result words (ascending) and the exclusive
-// prefix popcounts pre[k] (pre[words] = card) to o_idx/o_val/o_pre.
-__device__ __forceinline__ int warp_isect_out(const uint32_t *__restrict__ idx,
-                                              const uint32_t *__restrict__ val, int64_t a0,
-                                              int64_t a1, int64_t b0, int64_t b1,
-                                              uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
-  const int lane = lane_id();
-  if (a1 - a0 > b1 - b0) {
-    int64_t t0 = a0, t1 = a1;
-    a0 = b0; a1 = b1; b0 = t0; b1 = t1;
-  }
   int pos = 0, run = 0;
   int64_t lo = b0;
   for (int64_t base = a0; base < a1; base += 32) {
@@ -131,46 +131,617 @@ __device__ __forceinline__ int warp_isect_out(const uint32_t *__restrict__ idx,
     uint32_t x = 0, key = 0;
     if (i < a1) {
       key = __ldg(idx + i);
-      j = lower_bound_u32(idx, lo, b1, key);
-      if (j < b1 && __ldg(idx + j) == key) x = __ldg(val + i) & __ldg(val + j);
+      if (dense_b) {
+        x = __ldg(val + i) & __ldg(dense_b + key);
+        j = b0;
+      } else {
+        j = lower_bound_u32(idx, lo, b1, key);
+        if (j < b1 && __ldg(idx + j) == key) x = __ldg(val + i) & __ldg(val + j);
+      }
     }
     const unsigned nz = __ballot_sync(FULL, x != 0);
-    int c = __popc(x), incl = c;
+    const int c = __popc(x);
+    if (OUT) {
+      int incl = c;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (x) {
-      const int k = pos + __popc(nz & lanemask_lt());
-      o_idx[k] = key;
-      o_val[k] = x;
-      o_pre[k] = run + incl - c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (x) {
+        const int k = pos + __popc(nz & lanemask_lt());
+        o_idx[k] = key;
+        o_val[k] = x;
+        o_pre[k] = run + incl - c;
+      }
+      run += __shfl_sync(FULL, incl, 31);
+    } else {
+      run += __reduce_add_sync(FULL, c);
     }
     pos += __popc(nz);
-    run += __shfl_sync(FULL, incl, 31);
-    const int64_t jl = __shfl_sync(FULL, j, 31);
-    if (jl >= b1) break;
-    lo = jl;
+    if (!dense_b) {
+      const int64_t jl = __shfl_sync(FULL, j, 31);
+      if (jl >= b1) break;
+      lo = jl;
+    }
   }
-  if (lane == 0) o_pre[pos] = run;
-  __syncwarp();
+  if (OUT) {
+    if (lane == 0) o_pre[pos] = run;
+    __syncwarp();
+  }
+  card = run;
   return pos;
 }
 
-// Frame size in 32-bit words for a task-local universe.
-__host__ __device__ __forceinline__ int64_t frame_words(int nR, int nL, int wR, int wL, int p_eff,
-                                                        bool instr) {
+// adj[r] & adj[s] with the shorter side walked and the longer side probed.
+template <bool OUT>
+__device__ __forceinline__ int isect_adj(const Graph2 &g, int r, int s, int &card,
+                                         uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
+  int64_t a0 = g.aoff[r], a1 = g.aoff[r + 1], b0 = g.aoff[s], b1 = g.aoff[s + 1];
+  int lng = s;
+  if (a1 - a0 > b1 - b0) {
+    int64_t t0 = a0, t1 = a1;
+    a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+    lng = r;
+  }
+  const int sl = g.dense_id[lng];
+  const uint32_t *db = sl >= 0 ? g.dense + (int64_t)sl * g.mw : nullptr;
+  return warp_isect<OUT>(g.aidx, g.aval, a0, a1, b0, b1, db, card, o_idx, o_val, o_pre);
+}
+
+template <bool OUT>
+__device__ __forceinline__ int isect_dir(const Graph2 &g, int r, int s, int &card,
+                                         uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
+  int64_t a0 = g.doff[r], a1 = g.doff[r + 1], b0 = g.doff[s], b1 = g.doff[s + 1];
+  if (a1 - a0 > b1 - b0) {
+    int64_t t0 = a0, t1 = a1;
+    a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+  }
+  return warp_isect<OUT>(g.didx, g.dval, a0, a1, b0, b1, nullptr, card, o_idx, o_val, o_pre);
+}
+
+// Frame: the task-local universe.  The read-only part (built once) and the
+// per-warp DFS scratch are carved separately so split tasks can share the
+// former from global memory.
+struct Frame {
+  uint32_t *r_idx, *r_val;
+  int *r_pre;
+  uint32_t *l_idx, *l_val;
+  int *l_pre;
+  int *lids;
+  uint32_t *rowR, *rowL;
+  int *adjw, *dirw;
+  int *cand;
+  uint32_t *setR, *setL;
+  int *surv;
+  int *ns, *cur;
+};
+
+// rowL is materialised for p_eff >= 5 (reused at every depth) and for p_eff = 4
+// without a slot map; p_eff = 4 with a map walks dir2(u) lazily instead.
+__host__ __device__ __forceinline__ bool has_rowL(int p_eff, int map_words) {
+  return p_eff >= 5 || (p_eff == 4 && map_words == 0);
+}
+
+__host__ __device__ __forceinline__ int64_t ro_words(int nR, int nL, int wR, int wL, bool rowL,
+                                                     bool instr) {
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
-  const int64_t levels = p_eff - 2;
   int64_t w = 3 * (int64_t)wR + 1 + 3 * (int64_t)wL + 1;  // C_R1 / C_L1 HTB words + prefixes
   w += nL;                                                 // lids
   w += (int64_t)nL * WR;                                   // rowR
-  if (p_eff >= 4) w += (int64_t)nL * WL;                   // rowL
+  if (rowL) w += (int64_t)nL * WL;                         // rowL
   if (instr) w += 2 * (int64_t)nL;                         // adj / dir2 slice words
-  w += nL;                                                 // candidate compaction
-  w += levels * (WR + WL + nL + 2);                        // per-level R, L, survivors, ns/cur
-  return w;
+  return (w + 3) & ~int64_t(3);
+}
+
+__host__ __device__ __forceinline__ int64_t scratch_words(int nR, int nL, int p_eff) {
+  const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
+  const int64_t levels = p_eff - 2;
+  return ((int64_t)nL + levels * (WR + WL + nL + 2) + 3) & ~int64_t(3);
+}
+
+__device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d, bool rowL,
+                                         bool instr) {
+  f.r_idx = p; p += d.wR;
+  f.r_val = p; p += d.wR;
+  f.r_pre = (int *)p; p += d.wR + 1;
+  f.l_idx = p; p += d.wL;
+  f.l_val = p; p += d.wL;
+  f.l_pre = (int *)p; p += d.wL + 1;
+  f.lids = (int *)p; p += d.nL;
+  f.rowR = p; p += (int64_t)d.nL * d.WR;
+  f.rowL = p; if (rowL) p += (int64_t)d.nL * d.WL;
+  f.adjw = (int *)p; if (instr) p += d.nL;
+  f.dirw = (int *)p;
+}
+
+__device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims &d, int p_eff) {
+  const int levels = p_eff - 2;
+  f.cand = (int *)p; p += d.nL;
+  f.setR = p; p += (int64_t)levels * d.WR;
+  f.setL = p; p += (int64_t)levels * d.WL;
+  f.surv = (int *)p; p += (int64_t)levels * d.nL;
+  f.ns = (int *)p; p += levels;
+  f.cur = (int *)p;
+}
+
+// Writes a local-universe row whose set positions arrive in ascending order:
+// each 32-bit word is stored once, from a register, with no read-modify-write.
+struct RowWriter {
+  uint32_t *row;
+  int W, cur;
+  uint32_t bits;
+  __device__ __forceinline__ RowWriter(uint32_t *r, int w) : row(r), W(w), cur(0), bits(0) {}
+  __device__ __forceinline__ void flush_to(int w) {
+    row[cur] = bits;
+    for (int x = cur + 1; x < w; x++) row[x] = 0;
+    cur = w;
+    bits = 0;
+  }
+  __device__ __forceinline__ void set(int pos) {
+    const int w = pos >> 5;
+    if (w != cur) flush_to(w);
+    bits |= 1u << (pos & 31);
+  }
+  __device__ __forceinline__ void set_run(int pos, int len) {  // len <= 32
+    const int w = pos >> 5, sh = pos & 31;
+    if (w != cur) flush_to(w);
+    const unsigned long long x = (len == 32 ? 0xffffffffull : ((1ull << len) - 1ull)) << sh;
+    bits |= (uint32_t)x;
+    if (x >> 32) {
+      flush_to(w + 1);
+      bits = (uint32_t)(x >> 32);
+    }
+  }
+  // bits m (a subset of HTB word v whose first local index is pre)
+  __device__ __forceinline__ void add(int pre, uint32_t v, uint32_t m) {
+    if (m == v) {
+      set_run(pre, __popc(v));
+      return;
+    }
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      set(pre + __popc(v & ((1u << b) - 1u)));
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    if (W) flush_to(W);
+  }
+};
+
+// row = (local word list S) & (global HTB slice [g0,g1)), mapped to local bits.
+// Dense hub rows answer each S word with one load; short rows walk the shorter
+// side and bisect the longer (htb.py:122-154).
+__device__ __forceinline__ void local_row(const uint32_t *s_idx, const uint32_t *s_val,
+                                          const int *s_pre, int ns, const uint32_t *__restrict__ gidx,
+                                          const uint32_t *__restrict__ gval, int64_t g0, int64_t g1,
+                                          const uint32_t *__restrict__ dense_row, uint32_t *row,
+                                          int W) {
+  RowWriter rw(row, W);
+  if (dense_row) {
+    int k = 0;
+    for (; k + 4 <= ns; k += 4) {  // four independent probes in flight
+      uint32_t d[4];
+#pragma unroll
+      for (int t = 0; t < 4; t++) d[t] = __ldg(dense_row + s_idx[k + t]);
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const uint32_t m = s_val[k + t] & d[t];
+        if (m) rw.add(s_pre[k + t], s_val[k + t], m);
+      }
+    }
+    for (; k < ns; k++) {
+      const uint32_t m = s_val[k] & __ldg(dense_row + s_idx[k]);
+      if (m) rw.add(s_pre[k], s_val[k], m);
+    }
+  } else if (ns <= g1 - g0) {
+    int64_t lo = g0;
+    for (int k = 0; k < ns; k++) {
+      const uint32_t key = s_idx[k];
+      const int64_t j = lower_bound_u32(gidx, lo, g1, key);
+      if (j == g1) break;
+      if (__ldg(gidx + j) == key) {
+        const uint32_t m = s_val[k] & __ldg(gval + j);
+        if (m) rw.add(s_pre[k], s_val[k], m);
+        lo = j + 1;
+      } else {
+        lo = j;
+      }
+    }
+  } else {
+    int lo = 0;
+    for (int64_t j = g0; j < g1; j++) {
+      const uint32_t key = __ldg(gidx + j);
+      int a = lo, b = ns;
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if (s_idx[mid] < key) a = mid + 1;
+        else b = mid;
+      }
+      if (a == ns) break;
+      if (s_idx[a] == key) {
+        const uint32_t m = s_val[a] & __ldg(gval + j);
+        if (m) rw.add(s_pre[a], s_val[a], m);
+        lo = a + 1;
+      } else {
+        lo = a;
+      }
+    }
+  }
+  rw.finish();
+}
+
+// rowL via the anchor-word slot map: walk dir2(x)'s HTB words, one map lookup each.
+__device__ __forceinline__ void local_row_map(const uint16_t *map, const uint32_t *l_val,
+                                              const int *l_pre, const uint32_t *__restrict__ gidx,
+                                              const uint32_t *__restrict__ gval, int64_t g0,
+                                              int64_t g1, uint32_t *row, int W) {
+  RowWriter rw(row, W);
+  for (int64_t j = g0; j < g1; j++) {
+    const int k = map[__ldg(gidx + j)];
+    if (k != 0xffff) {
+      const uint32_t m = l_val[k] & __ldg(gval + j);
+      if (m) rw.add(l_pre[k], l_val[k], m);
+    }
+  }
+  rw.finish();
+}
+
+// Number of original HTB words (ranges [pre[k], pre[k+1])) a local bitset touches.
+__device__ __forceinline__ int words_touched(const uint32_t *set, const int *pre, int nwords,
+                                             int W, bool single) {
+  int c = 0;
+  if (single) {
+    for (int w = lane_id(); w < W; w += 32) c += __popc(set[w]);
+  } else {
+    for (int k = lane_id(); k < nwords; k += 32) {
+      const int a = pre[k], b = pre[k + 1];
+      const int w0 = a >> 5, w1 = (b - 1) >> 5;
+      unsigned long long x = set[w0];
+      if (w1 > w0) x |= (unsigned long long)set[w1] << 32;
+      x >>= (a & 31);
+      const int len = b - a;
+      const unsigned long long mask = len >= 64 ? ~0ull : ((1ull << len) - 1ull);
+      c += (x & mask) != 0;
+    }
+  }
+  return __reduce_add_sync(FULL, c);
+}
+
+// Same count for R & ru, by one lane.
+__device__ __forceinline__ int lane_words(const uint32_t *R, const uint32_t *ru, const int *pre,
+                                          int nwords, int W, bool single) {
+  int c = 0;
+  if (single) {
+    for (int w = 0; w < W; w++) c += __popc(R[w] & ru[w]);
+    return c;
+  }
+  for (int k = 0; k < nwords; k++) {
+    const int a = pre[k], b = pre[k + 1];
+    const int w0 = a >> 5, w1 = (b - 1) >> 5;
+    unsigned long long x = R[w0] & ru[w0];
+    if (w1 > w0) x |= (unsigned long long)(R[w1] & ru[w1]) << 32;
+    x >>= (a & 31);
+    const int len = b - a;
+    const unsigned long long mask = len >= 64 ? ~0ull : ((1ull << len) - 1ull);
+    c += (x & mask) != 0;
+  }
+  return c;
+}
+
+// order-preserving compaction of the set bits of a W-word set into cand[]
+__device__ __forceinline__ int compact_bits(const uint32_t *set, int W, int *cand) {
+  const int lane = lane_id();
+  int n = 0;
+  for (int w0 = 0; w0 < W; w0 += 32) {
+    const uint32_t mine = w0 + lane < W ? set[w0 + lane] : 0u;
+    unsigned nz = __ballot_sync(FULL, mine != 0);
+    while (nz) {
+      const int x = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t bits = __shfl_sync(FULL, mine, x);
+      if ((bits >> lane) & 1u) cand[n + __popc(bits & lanemask_lt())] = (w0 + x) * 32 + lane;
+      n += __popc(bits);
+    }
+  }
+  __syncwarp();
+  return n;
+}
+
+struct Tally {
+  unsigned long long batches = 0, inter = 0, opw = 0, minw = 0;
+};
+
+// reference batch count for one node expansion (engine.py:306-313, 329-331)
+__device__ __forceinline__ unsigned node_batches(const Params &P, unsigned ncand, int wr, int wl,
+                                                 bool leaf) {
+  if (!ncand) return 0;
+  if (P.mode_dfs) return ncand;
+  unsigned b = (unsigned)P.cap / (unsigned)(wr > 1 ? wr : 1);
+  if (!leaf) {
+    const unsigned b2 = (unsigned)P.cap / (unsigned)(wl > 1 ? wl : 1);
+    if (b2 < b) b = b2;
+  }
+  if (b < 1) b = 1;
+  return (ncand + b - 1) / b;
+}
+
+// Leaf-parent nodes, one per lane.  Node u (a survivor of the node at
+// `level`) has R' = R & rowR[u] and L' = L & rowL[u] -- or, with LAZY
+// (p_eff = 4, level 1), L' = dir2(u) & C_L1 walked through the slot map --
+// and its children are leaves: add C(|R' & rowR[w]|, q) for w in L'
+// (engine.py:342-347).  No warp synchronisation inside.
+template <bool INSTR, bool LAZY>
+__device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, const Dims &d,
+                                             int level, const int *list, int n,
+                                             const uint16_t *map, Acc128 &acc, Tally &tl) {
+  const int lane = lane_id();
+  const int WR = d.WR, WL = d.WL;
+  const uint32_t *R = f.setR + (level - 1) * WR;
+  const uint32_t *Ls = f.setL + (level - 1) * WL;
+  const int q = P.q_eff;
+  for (int i = lane; i < n; i += 32) {
+    const int u = list[i];
+    const uint32_t *ru = f.rowR + (int64_t)u * WR;
+    const int wr = lane_words(R, ru, f.r_pre, d.wR, WR, d.r_single);
+    const uint32_t r0 = WR == 1 ? (R[0] & ru[0]) : 0u;
+    unsigned ncand = 0;
+    auto leaf = [&](int w) {
+      const uint32_t *rw = f.rowR + (int64_t)w * WR;
+      int c;
+      if (WR == 1) c = __popc(r0 & rw[0]);
+      else {
+        c = 0;
+        for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
+      }
+      ncand++;
+      if (INSTR) {
+        tl.inter++;
+        tl.opw += wr + f.adjw[w];
+        tl.minw += wr < f.adjw[w] ? wr : f.adjw[w];
+      }
+      if (c >= q) add_comb(P, acc, c);
+    };
+    if (LAZY) {
+      const int id = f.lids[u];
+      const int64_t g0 = P.g.doff[id], g1 = P.g.doff[id + 1];
+      for (int64_t j = g0; j < g1; j++) {
+        const int k = map[__ldg(P.g.didx + j)];
+        if (k == 0xffff) continue;
+        const uint32_t v = f.l_val[k];
+        uint32_t m = v & __ldg(P.g.dval + j);
+        const int pre = f.l_pre[k];
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          leaf(pre + __popc(v & ((1u << b) - 1u)));
+        }
+      }
+    } else {
+      const uint32_t *rl = f.rowL + (int64_t)u * WL;
+      for (int x = 0; x < WL; x++) {
+        uint32_t m = Ls[x] & rl[x];
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          leaf(x * 32 + b);
+        }
+      }
+    }
+    tl.batches += node_batches(P, ncand, wr, 0, true);
+  }
+}
+
+// Expand node at `level` (1-based): children at level+1 (engine.py:315-374).
+// Children that are leaves are counted here; children that are leaf-parents
+// are finished lane-parallel (leaf_parents); deeper survivors are listed in
+// surv[level-1] for the depth-first descent.
+template <bool INSTR, bool LAZY>
+__device__ __forceinline__ void expand(const Params &P, const Frame &f, const Dims &d, int level,
+                                       const uint16_t *map, Acc128 &acc, Tally &tl) {
+  const int lane = lane_id();
+  const int WR = d.WR, WL = d.WL, nL = d.nL;
+  const int li = level - 1;
+  const uint32_t *R = f.setR + li * WR;
+  const uint32_t *Ls = f.setL + li * WL;
+  const bool leaf = level + 1 == P.p_eff - 1;
+  const bool lp = level + 1 == P.p_eff - 2;  // children are leaf-parents
+  const int ncand = compact_bits(Ls, WL, f.cand);
+  const int wr = level == 1 ? d.wR : words_touched(R, f.r_pre, d.wR, WR, d.r_single);
+  const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_pre, d.wL, WL, d.l_single));
+  if (lane == 0) tl.batches += node_batches(P, (unsigned)ncand, wr, wl, leaf);
+  int ns = 0;
+  const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
+  int *out = f.surv + li * nL;
+  for (int c0 = 0; c0 < ncand; c0 += 32) {
+    const int i = c0 + lane;
+    bool keep = false;
+    int u = 0;
+    if (i < ncand) {
+      u = f.cand[i];
+      const uint32_t *row = f.rowR + (int64_t)u * WR;
+      int cr = 0;
+      for (int w = 0; w < WR; w++) cr += __popc(R[w] & row[w]);
+      if (INSTR) {
+        tl.inter++;
+        tl.opw += wr + f.adjw[u];
+        tl.minw += wr < f.adjw[u] ? wr : f.adjw[u];
+      }
+      if (cr >= P.q_eff) {
+        if (leaf) {
+          add_comb(P, acc, cr);
+        } else {
+          if (INSTR) {
+            tl.inter++;
+            tl.opw += wl + f.dirw[u];
+            tl.minw += wl < f.dirw[u] ? wl : f.dirw[u];
+          }
+          if (LAZY) {
+            keep = true;  // |L'| >= 1 is checked when the leaf-parent is walked
+          } else {
+            const uint32_t *rl = f.rowL + (int64_t)u * WL;
+            int cl = 0;
+            for (int w = 0; w < WL; w++) cl += __popc(Ls[w] & rl[w]);
+            keep = cl >= need_l;
+          }
+        }
+      }
+    }
+    if (!leaf) {
+      const unsigned m = __ballot_sync(FULL, keep);
+      if (keep) out[ns + __popc(m & lanemask_lt())] = u;
+      ns += __popc(m);
+    }
+  }
+  __syncwarp();
+  if (lp && ns) {
+    leaf_parents<INSTR, LAZY>(P, f, d, level, out, ns, map, acc, tl);
+    ns = 0;
+  }
+  if (lane == 0) {
+    f.ns[li] = ns;
+    f.cur[li] = 0;
+  }
+  __syncwarp();
+}
+
+// Where split nodes go (heavy tasks only).
+struct SplitSink {
+  uint32_t *arena;          // sub-task records
+  int64_t arena_words;
+  unsigned long long *index; // record offsets
+  int64_t index_cap;
+  int level;                // emit nodes of this level instead of descending
+  int64_t frame_off;        // this task's read-only frame in the frame arena
+  int task_j;               // local task index
+};
+
+// Push node (level lv, sets R, L) as a sub-task; false if the arena is full.
+__device__ __forceinline__ bool emit_node(const Params &P, const SplitSink &S, const Dims &d,
+                                          int lv, const uint32_t *R, const uint32_t *rr,
+                                          const uint32_t *Ls, const uint32_t *rl) {
+  const int lane = lane_id();
+  const int64_t words = 4 + d.WR + d.WL;
+  long long off = -1;
+  if (lane == 0) {
+    const unsigned long long o = atomicAdd(P.ctr + CTR_SUB_USED, (unsigned long long)words);
+    if ((int64_t)(o + words) <= S.arena_words) {
+      const unsigned long long k = atomicAdd(P.ctr + CTR_SUB_N, 1ull);
+      if ((int64_t)k < S.index_cap) {
+        off = (long long)o;
+        S.index[k] = o;
+      }
+    }
+  }
+  off = __shfl_sync(FULL, off, 0);
+  if (off < 0) return false;
+  uint32_t *rec = S.arena + off;
+  if (lane == 0) {
+    rec[0] = (uint32_t)S.task_j;
+    rec[1] = (uint32_t)lv;
+    rec[2] = (uint32_t)(S.frame_off & 0xffffffffll);
+    rec[3] = (uint32_t)(S.frame_off >> 32);
+  }
+  for (int w = lane; w < d.WR; w += 32) rec[4 + w] = R[w] & rr[w];
+  for (int w = lane; w < d.WL; w += 32) rec[4 + d.WR + w] = Ls[w] & rl[w];
+  __syncwarp();
+  return true;
+}
+
+// DFS from a node at `start` whose sets sit in setR/setL[start-1].
+template <bool INSTR, bool LAZY>
+__device__ __forceinline__ void dfs(const Params &P, const Frame &f, const Dims &d, int start,
+                                    const uint16_t *map, Acc128 &acc, Tally &tl,
+                                    const SplitSink *sink) {
+  const int lane = lane_id();
+  const int WR = d.WR, WL = d.WL, nL = d.nL, p_eff = P.p_eff;
+  expand<INSTR, LAZY>(P, f, d, start, map, acc, tl);
+  int level = start;
+  while (level >= start) {
+    const int li = level - 1;
+    if (level + 1 < p_eff - 2 && f.cur[li] < f.ns[li]) {
+      const int u = f.surv[li * nL + f.cur[li]];
+      __syncwarp();
+      if (lane == 0) f.cur[li]++;
+      const uint32_t *rr = f.rowR + (int64_t)u * WR;
+      const uint32_t *rl = f.rowL + (int64_t)u * WL;
+      if (sink && level + 1 == sink->level &&
+          emit_node(P, *sink, d, level + 1, f.setR + li * WR, rr, f.setL + li * WL, rl))
+        continue;
+      for (int w = lane; w < WR; w += 32) f.setR[(li + 1) * WR + w] = f.setR[li * WR + w] & rr[w];
+      for (int w = lane; w < WL; w += 32) f.setL[(li + 1) * WL + w] = f.setL[li * WL + w] & rl[w];
+      __syncwarp();
+      level++;
+      expand<INSTR, LAZY>(P, f, d, level, map, acc, tl);
+    } else {
+      level--;
+    }
+  }
+}
+
+// Build the read-only frame of task (r, s) at f (engine.py:277-292, 338, 360).
+// With a slot map the map is left filled for the DFS (the caller clears it).
+template <bool INSTR, bool LAZY>
+__device__ __forceinline__ void build_frame(const Params &P, const Frame &f, const Dims &d, int r,
+                                            int s, uint16_t *map) {
+  const int lane = lane_id();
+  int card;
+  isect_adj<true>(P.g, r, s, card, f.r_idx, f.r_val, f.r_pre);
+  isect_dir<true>(P.g, r, s, card, f.l_idx, f.l_val, f.l_pre);
+  // decode C_L1 ids (ascending, htb.py:42-52); fill the slot map
+  for (int k = lane; k < d.wL; k += 32) {
+    uint32_t v = f.l_val[k];
+    const int base_id = (int)f.l_idx[k] * 32;
+    int pos = f.l_pre[k];
+    if (map) map[f.l_idx[k]] = (uint16_t)k;
+    while (v) {
+      f.lids[pos++] = base_id + __ffs(v) - 1;
+      v &= v - 1;
+    }
+  }
+  __syncwarp();
+  for (int x = lane; x < d.nL; x += 32) {
+    const int id = f.lids[x];
+    const int64_t a0 = P.g.aoff[id], a1 = P.g.aoff[id + 1];
+    const int sl = P.g.dense_id[id];
+    local_row(f.r_idx, f.r_val, f.r_pre, d.wR, P.g.aidx, P.g.aval, a0, a1,
+              sl >= 0 ? P.g.dense + (int64_t)sl * P.g.mw : nullptr, f.rowR + (int64_t)x * d.WR,
+              d.WR);
+    const int64_t d0 = P.g.doff[id], d1 = P.g.doff[id + 1];
+    if (P.p_eff >= 4 && !LAZY) {
+      if (map)
+        local_row_map(map, f.l_val, f.l_pre, P.g.didx, P.g.dval, d0, d1,
+                      f.rowL + (int64_t)x * d.WL, d.WL);
+      else
+        local_row(f.l_idx, f.l_val, f.l_pre, d.wL, P.g.didx, P.g.dval, d0, d1, nullptr,
+                  f.rowL + (int64_t)x * d.WL, d.WL);
+    }
+    if (INSTR) {
+      f.adjw[x] = (int)(a1 - a0);
+      f.dirw[x] = (int)(d1 - d0);
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void clear_map(uint16_t *map, const Frame &f, const Dims &d) {
+  if (!map) return;
+  for (int k = lane_id(); k < d.wL; k += 32) map[f.l_idx[k]] = 0xffff;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void init_root_sets(const Frame &f, const Dims &d) {
+  const int lane = lane_id();
+  for (int w = lane; w < d.WR; w += 32) {
+    const int rem = d.nR - w * 32;
+    f.setR[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
+  }
+  for (int w = lane; w < d.WL; w += 32) {
+    const int rem = d.nL - w * 32;
+    f.setL[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -207,16 +778,14 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nloc = P.n_tasks > P.shard ? (P.n_tasks - P.shard + P.nshards - 1) / P.nshards : 0;
   Acc128 a{0, 0};
-  unsigned long long alive = 0, inter = 0, opw = 0, minw = 0, maxneed = 0;
+  unsigned long long alive = 0, inter = 0, opw = 0, minw = 0, maxro = 0, maxscr = 0;
   for (int64_t j = gw; j < nloc; j += nw) {
     const int64_t t = P.shard + j * P.nshards;
     const int2 tk = P.tasks[t];
-    const int64_t ra0 = P.g.aoff[tk.x], ra1 = P.g.aoff[tk.x + 1];
-    const int64_t sa0 = P.g.aoff[tk.y], sa1 = P.g.aoff[tk.y + 1];
-    int cr, wr;
-    warp_isect_count(P.g.aidx, P.g.aval, ra0, ra1, sa0, sa1, cr, wr);
+    int cr;
+    const int wr = isect_adj<false>(P.g, tk.x, tk.y, cr, nullptr, nullptr, nullptr);
     if (INSTR) {
-      const int64_t la = ra1 - ra0, lb = sa1 - sa0;
+      const int64_t la = P.g.aoff[tk.x + 1] - P.g.aoff[tk.x], lb = P.g.aoff[tk.y + 1] - P.g.aoff[tk.y];
       inter++;
       opw += la + lb;
       minw += la < lb ? la : lb;
@@ -228,12 +797,10 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
       if (P.p_eff == 2) {
         add_comb(P, one, cr);
       } else {
-        const int64_t rd0 = P.g.doff[tk.x], rd1 = P.g.doff[tk.x + 1];
-        const int64_t sd0 = P.g.doff[tk.y], sd1 = P.g.doff[tk.y + 1];
-        int cl, wl;
-        warp_isect_count(P.g.didx, P.g.dval, rd0, rd1, sd0, sd1, cl, wl);
+        int cl;
+        const int wl = isect_dir<false>(P.g, tk.x, tk.y, cl, nullptr, nullptr, nullptr);
         if (INSTR) {
-          const int64_t la = rd1 - rd0, lb = sd1 - sd0;
+          const int64_t la = P.g.doff[tk.x + 1] - P.g.doff[tk.x], lb = P.g.doff[tk.y + 1] - P.g.doff[tk.y];
           inter++;
           opw += la + lb;
           minw += la < lb ? la : lb;
@@ -244,8 +811,11 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
           const unsigned long long c = (unsigned long long)cl * (unsigned long long)cr;
           key = c > 0xfffffffeull ? 0xffffffffu : (uint32_t)(c ? c : 1);
           alive++;
-          const int64_t need = frame_words(cr, cl, wr, wl, P.p_eff, INSTR);
-          if ((unsigned long long)need > maxneed) maxneed = need;
+          const unsigned long long ro =
+              ro_words(cr, cl, wr, wl, has_rowL(P.p_eff, P.map_words), INSTR);
+          const unsigned long long sc = scratch_words(cr, cl, P.p_eff);
+          maxro = ro > maxro ? ro : maxro;
+          maxscr = sc > maxscr ? sc : maxscr;
         }
       }
     }
@@ -267,338 +837,56 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
       atomicAdd(P.ctr + CTR_OPW, opw);
       atomicAdd(P.ctr + CTR_MINW, minw);
     }
-    if (maxneed) atomicMax(P.ctr + CTR_MAXNEED, maxneed);
+    if (maxro) atomicMax(P.ctr + CTR_MAXRO, maxro);
+    if (maxscr) atomicMax(P.ctr + CTR_MAXSCR, maxscr);
   }
 }
 
 // ---------------------------------------------------------------------------
 // enumeration (engine.py:315-374) over the task-local universe
 // ---------------------------------------------------------------------------
-struct Frame {
-  uint32_t *r_idx, *r_val;
-  int *r_pre;
-  uint32_t *l_idx, *l_val;
-  int *l_pre;
-  int *lids;
-  uint32_t *rowR, *rowL;
-  int *adjw, *dirw;
-  int *cand;
-  uint32_t *setR, *setL;
-  int *surv;
-  int *ns, *cur;
+struct EnumArgs {
+  const Info *__restrict__ info;
+  const int32_t *__restrict__ queue;  // local task ids, LPT order
+  int64_t n_alive;
+  int64_t n_heavy;                    // queue[0, n_heavy) are split
+  int budget_words;                   // shared memory per warp for frames
+  uint32_t *gscratch;                 // per-warp global fallback
+  int64_t gscratch_words;
+  uint32_t *frames;                   // heavy read-only frames
+  const int64_t *frame_off;           // [n_heavy]
+  SplitSink sink;
 };
 
-__device__ __forceinline__ Frame carve(uint32_t *base, int nR, int nL, int wR, int wL, int p_eff,
-                                       bool instr) {
-  const int WR = (nR + 31) >> 5, WL = (nL + 31) >> 5, levels = p_eff - 2;
-  Frame f;
-  uint32_t *p = base;
-  f.r_idx = p; p += wR;
-  f.r_val = p; p += wR;
-  f.r_pre = (int *)p; p += wR + 1;
-  f.l_idx = p; p += wL;
-  f.l_val = p; p += wL;
-  f.l_pre = (int *)p; p += wL + 1;
-  f.lids = (int *)p; p += nL;
-  f.rowR = p; p += (int64_t)nL * WR;
-  f.rowL = p; if (p_eff >= 4) p += (int64_t)nL * WL;
-  f.adjw = (int *)p; if (instr) p += nL;
-  f.dirw = (int *)p; if (instr) p += nL;
-  f.cand = (int *)p; p += nL;
-  f.setR = p; p += (int64_t)levels * WR;
-  f.setL = p; p += (int64_t)levels * WL;
-  f.surv = (int *)p; p += (int64_t)levels * nL;
-  f.ns = (int *)p; p += levels;
-  f.cur = (int *)p; p += levels;
-  return f;
-}
-
-// OR the bits m (a subset of v) of HTB word (v, local start pre) into row.
-__device__ __forceinline__ void scatter_local(uint32_t *row, int pre, uint32_t v, uint32_t m) {
-  while (m) {
-    const int b = __ffs(m) - 1;
-    m &= m - 1;
-    const int pos = pre + __popc(v & ((1u << b) - 1u));
-    row[pos >> 5] |= 1u << (pos & 31);
-  }
-}
-
-// row = (local word list S) & (global HTB slice [g0,g1)), mapped to local bits.
-// Walks the shorter side and bisects the longer (htb.py:122-154).
-__device__ __forceinline__ void local_row(const uint32_t *s_idx, const uint32_t *s_val,
-                                          const int *s_pre, int ns, const uint32_t *__restrict__ gidx,
-                                          const uint32_t *__restrict__ gval, int64_t g0, int64_t g1,
-                                          uint32_t *row, int W) {
-  for (int w = 0; w < W; w++) row[w] = 0;
-  if (ns <= g1 - g0) {
-    int64_t lo = g0;
-    for (int k = 0; k < ns; k++) {
-      const uint32_t key = s_idx[k];
-      const int64_t j = lower_bound_u32(gidx, lo, g1, key);
-      if (j == g1) break;
-      if (__ldg(gidx + j) == key) {
-        const uint32_t m = s_val[k] & __ldg(gval + j);
-        if (m) scatter_local(row, s_pre[k], s_val[k], m);
-        lo = j + 1;
-      } else {
-        lo = j;
-      }
-    }
-  } else {
-    int lo = 0;
-    for (int64_t j = g0; j < g1; j++) {
-      const uint32_t key = __ldg(gidx + j);
-      int a = lo, b = ns;
-      while (a < b) {
-        const int mid = (a + b) >> 1;
-        if (s_idx[mid] < key) a = mid + 1;
-        else b = mid;
-      }
-      if (a == ns) break;
-      if (s_idx[a] == key) {
-        const uint32_t m = s_val[a] & __ldg(gval + j);
-        if (m) scatter_local(row, s_pre[a], s_val[a], m);
-        lo = a + 1;
-      } else {
-        lo = a;
-      }
-    }
-  }
-}
-
-// Number of original HTB words (ranges [pre[k], pre[k+1])) a local bitset touches.
-__device__ __forceinline__ int words_touched(const uint32_t *set, const int *pre, int nwords) {
-  int c = 0;
-  for (int k = lane_id(); k < nwords; k += 32) {
-    const int a = pre[k], b = pre[k + 1];
-    const int w0 = a >> 5, w1 = (b - 1) >> 5;
-    unsigned long long x = set[w0];
-    if (w1 > w0) x |= (unsigned long long)set[w1] << 32;
-    x >>= (a & 31);
-    const int len = b - a;
-    const unsigned long long mask = len >= 64 ? ~0ull : ((1ull << len) - 1ull);
-    c += (x & mask) != 0;
-  }
-  return __reduce_add_sync(FULL, c);
-}
-
-// popcount of a W-word set held in frame memory (warp-cooperative)
-__device__ __forceinline__ int set_card(const uint32_t *set, int W) {
-  int c = 0;
-  for (int w = lane_id(); w < W; w += 32) c += __popc(set[w]);
-  return __reduce_add_sync(FULL, c);
-}
-
-// order-preserving compaction of the set bits of a W-word set into cand[]
-__device__ __forceinline__ int compact_bits(const uint32_t *set, int W, int *cand) {
-  const int lane = lane_id();
-  int n = 0;
-  for (int w = 0; w < W; w++) {
-    const uint32_t bits = set[w];
-    if (!bits) continue;
-    if ((bits >> lane) & 1u) cand[n + __popc(bits & lanemask_lt())] = w * 32 + lane;
-    n += __popc(bits);
-  }
-  __syncwarp();
-  return n;
-}
-
-template <bool INSTR>
-struct Tally {
-  unsigned long long batches = 0, inter = 0, opw = 0, minw = 0;
-};
-
-// Expand node at `level` (1-based): children at level+1 (engine.py:315-374).
-template <bool INSTR>
-__device__ __forceinline__ void expand(const Params &P, const Frame &f, int level, int nR, int nL,
-                                       int wR1, int wL1, Acc128 &acc, Tally<INSTR> &tl) {
-  const int lane = lane_id();
-  const int WR = (nR + 31) >> 5, WL = (nL + 31) >> 5;
-  const int li = level - 1;
-  const uint32_t *R = f.setR + li * WR;
-  const uint32_t *Ls = f.setL + li * WL;
-  const bool leaf = level + 1 == P.p_eff - 1;
-  const int ncand = compact_bits(Ls, WL, f.cand);
-  // reference batch accounting (engine.py:306-313, 329-331)
-  const int wr = level == 1 ? wR1 : words_touched(R, f.r_pre, wR1);
-  const int wl = leaf ? 0 : (level == 1 ? wL1 : words_touched(Ls, f.l_pre, wL1));
-  if (lane == 0 && ncand) {
-    long long b = 1;
-    if (!P.mode_dfs) {
-      b = P.cap / (wr > 1 ? wr : 1);
-      if (!leaf) {
-        long long b2 = P.cap / (wl > 1 ? wl : 1);
-        if (b2 < b) b = b2;
-      }
-      if (b < 1) b = 1;
-    }
-    tl.batches += (ncand + b - 1) / b;
-  }
-  int ns = 0;
-  const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
-  for (int c0 = 0; c0 < ncand; c0 += 32) {
-    const int i = c0 + lane;
-    bool keep = false;
-    int u = 0;
-    if (i < ncand) {
-      u = f.cand[i];
-      const uint32_t *row = f.rowR + (int64_t)u * WR;
-      int cr = 0;
-      for (int w = 0; w < WR; w++) cr += __popc(R[w] & row[w]);
-      if (INSTR) {
-        tl.inter++;
-        tl.opw += wr + f.adjw[u];
-        tl.minw += wr < f.adjw[u] ? wr : f.adjw[u];
-      }
-      if (cr >= P.q_eff) {
-        if (leaf) {
-          add_comb(P, acc, cr);
-        } else {
-          const uint32_t *rl = f.rowL + (int64_t)u * WL;
-          int cl = 0;
-          for (int w = 0; w < WL; w++) cl += __popc(Ls[w] & rl[w]);
-          if (INSTR) {
-            tl.inter++;
-            tl.opw += wl + f.dirw[u];
-            tl.minw += wl < f.dirw[u] ? wl : f.dirw[u];
-          }
-          keep = cl >= need_l;
-        }
-      }
-    }
-    if (!leaf) {
-      const unsigned m = __ballot_sync(FULL, keep);
-      if (keep) f.surv[li * nL + ns + __popc(m & lanemask_lt())] = u;
-      ns += __popc(m);
-    }
-  }
-  if (lane == 0) {
-    f.ns[li] = ns;
-    f.cur[li] = 0;
-  }
-  __syncwarp();
-}
-
-template <bool INSTR>
-__global__ void __launch_bounds__(256) enum_kernel(Params P, const Info *__restrict__ info,
-                                                   const int32_t *__restrict__ queue,
-                                                   int64_t n_alive, int budget_words,
-                                                   uint32_t *__restrict__ gscratch,
-                                                   int64_t gscratch_words) {
-  extern __shared__ uint32_t smem[];
-  const int lane = lane_id();
-  const int wib = threadIdx.x >> 5;
-  const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  uint32_t *my_smem = smem + (int64_t)wib * budget_words;
-  uint32_t *my_global = gscratch ? gscratch + gwarp * gscratch_words : nullptr;
-  Acc128 total{0, 0};
-  Tally<INSTR> tl;
-  unsigned long long claims = 0, spills = 0;
-  const int p_eff = P.p_eff;
-  for (;;) {
-    long long qi = 0;
-    if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
-    qi = __shfl_sync(FULL, qi, 0);
-    if (qi >= n_alive) break;
-    claims++;
-    const int j = queue[qi];
-    const int64_t t = P.shard + (int64_t)j * P.nshards;
-    const int2 tk = P.tasks[t];
-    const Info in = info[j];
-    const int nR = in.cr, nL = in.cl, wR1 = in.wr, wL1 = in.wl;
-    const int WR = (nR + 31) >> 5, WL = (nL + 31) >> 5;
-    const int64_t need = frame_words(nR, nL, wR1, wL1, p_eff, INSTR);
-    uint32_t *base;
-    if (need <= budget_words) {
-      base = my_smem;
-    } else {
-      base = my_global;
-      spills++;
-      if (!base || need > gscratch_words) {  // cannot happen: sized from level-1 maxima
-        atomicExch(P.overflow, 2);
-        continue;
-      }
-    }
-    const Frame f = carve(base, nR, nL, wR1, wL1, p_eff, INSTR);
-    // re-materialise C_R1, C_L1 (engine.py:277-292)
-    warp_isect_out(P.g.aidx, P.g.aval, P.g.aoff[tk.x], P.g.aoff[tk.x + 1], P.g.aoff[tk.y],
-                   P.g.aoff[tk.y + 1], f.r_idx, f.r_val, f.r_pre);
-    warp_isect_out(P.g.didx, P.g.dval, P.g.doff[tk.x], P.g.doff[tk.x + 1], P.g.doff[tk.y],
-                   P.g.doff[tk.y + 1], f.l_idx, f.l_val, f.l_pre);
-    // decode C_L1 ids (ascending, htb.py:42-52)
-    for (int k = lane; k < wL1; k += 32) {
-      uint32_t v = f.l_val[k];
-      const int base_id = (int)f.l_idx[k] * 32;
-      int pos = f.l_pre[k];
-      while (v) {
-        f.lids[pos++] = base_id + __ffs(v) - 1;
-        v &= v - 1;
-      }
-    }
-    __syncwarp();
-    // task-local rows
-    for (int x = lane; x < nL; x += 32) {
-      const int id = f.lids[x];
-      const int64_t a0 = P.g.aoff[id], a1 = P.g.aoff[id + 1];
-      local_row(f.r_idx, f.r_val, f.r_pre, wR1, P.g.aidx, P.g.aval, a0, a1,
-                f.rowR + (int64_t)x * WR, WR);
-      const int64_t d0 = P.g.doff[id], d1 = P.g.doff[id + 1];
-      if (p_eff >= 4)
-        local_row(f.l_idx, f.l_val, f.l_pre, wL1, P.g.didx, P.g.dval, d0, d1,
-                  f.rowL + (int64_t)x * WL, WL);
-      if (INSTR) {
-        f.adjw[x] = (int)(a1 - a0);
-        f.dirw[x] = (int)(d1 - d0);
-      }
-    }
-    // level-1 node: C_R1, C_L1 = all local ids
-    for (int w = lane; w < WR; w += 32) {
-      const int rem = nR - w * 32;
-      f.setR[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
-    }
-    for (int w = lane; w < WL; w += 32) {
-      const int rem = nL - w * 32;
-      f.setL[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
-    }
-    __syncwarp();
-    Acc128 acc{0, 0};
-    expand<INSTR>(P, f, 1, nR, nL, wR1, wL1, acc, tl);
-    int level = 1;
-    while (level >= 1) {
-      const int li = level - 1;
-      if (level + 1 < p_eff - 1 && f.cur[li] < f.ns[li]) {
-        const int u = f.surv[li * nL + f.cur[li]];
-        __syncwarp();
-        if (lane == 0) f.cur[li]++;
-        const uint32_t *rr = f.rowR + (int64_t)u * WR;
-        const uint32_t *rl = f.rowL + (int64_t)u * WL;
-        for (int w = lane; w < WR; w += 32) f.setR[(li + 1) * WR + w] = f.setR[li * WR + w] & rr[w];
-        for (int w = lane; w < WL; w += 32) f.setL[(li + 1) * WL + w] = f.setL[li * WL + w] & rl[w];
-        __syncwarp();
-        level++;
-        expand<INSTR>(P, f, level, nR, nL, wR1, wL1, acc, tl);
-      } else {
-        level--;
-      }
-    }
-    acc = warp_sum128(acc);
-    if (lane == 0) {
-      total.add(acc.lo, acc.hi);
-      if (P.task_counts) {
+__device__ __forceinline__ void finish_task(const Params &P, Acc128 acc, int64_t t, bool atomic,
+                                            Acc128 &total) {
+  acc = warp_sum128(acc);
+  if (lane_id() == 0) {
+    total.add(acc.lo, acc.hi);
+    if (P.task_counts) {
+      if (atomic) atomic_add128(P.task_counts + 2 * t, P.overflow, acc.lo, acc.hi);
+      else {
         P.task_counts[2 * t] = acc.lo;
         P.task_counts[2 * t + 1] = acc.hi;
       }
     }
-    __syncwarp();
   }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void flush_tallies(const Params &P, const Acc128 &total, const Tally &tl,
+                                              unsigned long long claims, unsigned long long spills,
+                                              bool instr) {
+  const int lane = lane_id();
+  const unsigned long long batches = warp_sum(tl.batches);  // leaf_parents tally per lane
   if (lane == 0) {
     atomic_add128(P.acc, P.overflow, total.lo, total.hi);
-    atomicAdd(P.ctr + CTR_BATCHES, tl.batches);
+    atomicAdd(P.ctr + CTR_BATCHES, batches);
     if (claims > 1) atomicAdd(P.ctr + CTR_STOLEN, claims - 1);
     if (spills) atomicAdd(P.ctr + CTR_SPILL, spills);
   }
-  if (INSTR) {
-    unsigned long long a = warp_sum(tl.inter), b = warp_sum(tl.opw), c = warp_sum(tl.minw);
+  if (instr) {
+    const unsigned long long a = warp_sum(tl.inter), b = warp_sum(tl.opw), c = warp_sum(tl.minw);
     if (lane == 0) {
       atomicAdd(P.ctr + CTR_INTER, a);
       atomicAdd(P.ctr + CTR_OPW, b);
@@ -607,9 +895,138 @@ __global__ void __launch_bounds__(256) enum_kernel(Params P, const Info *__restr
   }
 }
 
+constexpr int ENUM_THREADS = 256;
+
+template <bool INSTR, bool LAZY>
+__global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArgs A) {
+  extern __shared__ uint32_t smem[];
+  const int lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int map_w = (P.map_words + 1) / 2;  // u16 entries packed in words
+  uint32_t *my = smem + (int64_t)wib * (map_w + A.budget_words);
+  uint16_t *map = P.map_words ? (uint16_t *)my : nullptr;
+  uint32_t *my_smem = my + map_w;
+  uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
+  if (map)
+    for (int i = lane; i < map_w; i += 32) my[i] = 0xffffffffu;
+  __syncwarp();
+  Acc128 total{0, 0};
+  Tally tl;
+  unsigned long long claims = 0, spills = 0;
+  const int p_eff = P.p_eff;
+  for (;;) {
+    long long qi = 0;
+    if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
+    qi = __shfl_sync(FULL, qi, 0);
+    if (qi >= A.n_alive) break;
+    claims++;
+    const int j = A.queue[qi];
+    const int64_t t = P.shard + (int64_t)j * P.nshards;
+    const int2 tk = P.tasks[t];
+    const Dims d = dims_of(A.info[j]);
+    const bool heavy = qi < A.n_heavy;
+    const bool rowL = heavy || has_rowL(p_eff, P.map_words);
+    const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, rowL, INSTR);
+    const int64_t sc = scratch_words(d.nR, d.nL, p_eff);
+    Frame f;
+    uint32_t *ro_base, *sc_base;
+    if (heavy) {
+      ro_base = A.frames + A.frame_off[qi];
+      if (sc <= A.budget_words) sc_base = my_smem;
+      else { sc_base = my_global; spills++; }
+    } else if (ro + sc <= A.budget_words) {
+      ro_base = my_smem;
+      sc_base = my_smem + ro;
+    } else {
+      ro_base = my_global;
+      sc_base = my_global + ro;
+      spills++;
+    }
+    if (!sc_base || (sc_base == my_global && (heavy ? sc : ro + sc) > A.gscratch_words)) {
+      if (lane == 0) atomicExch(P.overflow, 2);  // cannot happen: sized from level-1 maxima
+      continue;
+    }
+    carve_ro(f, ro_base, d, rowL, INSTR);
+    carve_scratch(f, sc_base, d, p_eff);
+    build_frame<INSTR, LAZY>(P, f, d, tk.x, tk.y, map);
+    init_root_sets(f, d);
+    Acc128 acc{0, 0};
+    if (heavy) {
+      SplitSink sink = A.sink;
+      sink.frame_off = A.frame_off[qi];
+      sink.task_j = j;
+      dfs<INSTR, false>(P, f, d, 1, map, acc, tl, &sink);
+    } else {
+      dfs<INSTR, LAZY>(P, f, d, 1, map, acc, tl, nullptr);
+    }
+    clear_map(map, f, d);
+    finish_task(P, acc, t, heavy, total);
+  }
+  flush_tallies(P, total, tl, claims, spills, INSTR);
+}
+
+// Split nodes of heavy tasks: warp per sub-task record.
+template <bool INSTR>
+__global__ void __launch_bounds__(ENUM_THREADS, 2) sub_kernel(Params P, EnumArgs A, int64_t n_sub) {
+  extern __shared__ uint32_t smem[];
+  const int lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  uint32_t *my_smem = smem + (int64_t)wib * A.budget_words;
+  uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
+  Acc128 total{0, 0};
+  Tally tl;
+  unsigned long long spills = 0;
+  const int p_eff = P.p_eff;
+  for (;;) {
+    long long k = 0;
+    if (lane == 0) k = (long long)atomicAdd(P.ctr + CTR_SUB_NEXT, 1ull);
+    k = __shfl_sync(FULL, k, 0);
+    if (k >= n_sub) break;
+    const uint32_t *rec = A.sink.arena + A.sink.index[k];
+    const int j = (int)rec[0];
+    const int lv = (int)rec[1];
+    const int64_t foff = (int64_t)rec[2] | ((int64_t)rec[3] << 32);
+    const int64_t t = P.shard + (int64_t)j * P.nshards;
+    const Dims d = dims_of(A.info[j]);
+    const int64_t sc = scratch_words(d.nR, d.nL, p_eff);
+    uint32_t *sc_base = sc <= A.budget_words ? my_smem : my_global;
+    if (sc_base == my_global) spills++;
+    if (!sc_base || (sc_base == my_global && sc > A.gscratch_words)) {
+      if (lane == 0) atomicExch(P.overflow, 2);
+      continue;
+    }
+    Frame f;
+    carve_ro(f, A.frames + foff, d, true, INSTR);
+    carve_scratch(f, sc_base, d, p_eff);
+    for (int w = lane; w < d.WR; w += 32) f.setR[(lv - 1) * d.WR + w] = rec[4 + w];
+    for (int w = lane; w < d.WL; w += 32) f.setL[(lv - 1) * d.WL + w] = rec[4 + d.WR + w];
+    __syncwarp();
+    Acc128 acc{0, 0};
+    dfs<INSTR, false>(P, f, d, lv, nullptr, acc, tl, nullptr);
+    finish_task(P, acc, t, true, total);
+  }
+  flush_tallies(P, total, tl, 0, spills, INSTR);
+}
+
 __global__ void iota32(int32_t *a, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) a[i] = (int32_t)i;
+}
+
+// frame / sub-task sizing for the heavy head of the queue
+__global__ void heavy_sizes(const Info *info, const int32_t *queue, int64_t n_heavy, int p_eff,
+                            bool instr, int split_level, int64_t *ro, int64_t *sub,
+                            unsigned long long *max_scr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_heavy) return;
+  const Info in = info[queue[i]];
+  ro[i] = ro_words(in.cr, in.cl, in.wr, in.wl, true, instr);
+  const int64_t WR = (in.cr + 31) / 32, WL = (in.cl + 31) / 32;
+  const int64_t nodes = split_level == 2 ? in.cl : (int64_t)in.cl * (in.cl - 1) / 2;
+  sub[i] = nodes * (4 + WR + WL);
+  atomicMax(max_scr, (unsigned long long)scratch_words(in.cr, in.cl, p_eff));
 }
 
 // C(c, q) for c <= max_deg as exact u128; returns first c whose value needs > 128 bits.
@@ -636,6 +1053,21 @@ int64_t binomials(int q, int max_deg, std::vector<ulonglong2> &out) {
   return first_bad;
 }
 
+template <typename T>
+T sum_device(const T *p, int64_t n, cudaStream_t st) {
+  DBuf<T> out;
+  out.alloc(1, st);
+  size_t tmp = 0;
+  BC_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, p, out.p, n, st));
+  DBuf<char> t;
+  t.alloc(tmp, st);
+  BC_CUDA(cub::DeviceReduce::Sum(t.p, tmp, p, out.p, n, st));
+  T h;
+  copy_d2h(&h, out.p, sizeof(T), st);
+  BC_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
 }  // namespace
 
 void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
@@ -644,6 +1076,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   BC_CUDA(cudaGetDevice(&device));
   const int sms = num_sms(device);
   const bool instr = (cfg.flags & BC_FLAG_INSTRUMENT) != 0;
+  const bool allow_split = (cfg.flags & BC_FLAG_NO_SPLIT) == 0;
   const int nshards = cfg.shard_count > 0 ? cfg.shard_count : 1;
   const int shard = cfg.shard_index;
   if (shard < 0 || shard >= nshards) throw Error(BC_EINVAL, "shard_index out of range");
@@ -672,7 +1105,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     tcounts.zero();
   }
   Params P;
-  P.g = Graph2{s.hadj_off.p, s.hadj_idx.p, s.hadj_val.p, s.hdir_off.p, s.hdir_idx.p, s.hdir_val.p};
+  P.g = Graph2{s.hadj_off.p, s.hadj_idx.p, s.hadj_val.p, s.hdir_off.p, s.hdir_idx.p, s.hdir_val.p,
+               s.dense_id.p, s.dense.p, s.dense_mw};
   P.tasks = s.tasks.p;
   P.n_tasks = n_tasks;
   P.shard = shard;
@@ -687,13 +1121,16 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.overflow = ovf.p;
   P.ctr = ctr.p;
   P.task_counts = want_tc ? tcounts.p : nullptr;
+  // slot map over anchor words for rowL (u16 per word) when it is small
+  const int64_t anchor_words = (s.n + 31) / 32;
+  P.map_words = (s.p_eff >= 4 && anchor_words <= 4096) ? (int)((anchor_words + 1) & ~1) : 0;
 
   cudaEvent_t e0, e1, e2;
   BC_CUDA(cudaEventCreate(&e0));
   BC_CUDA(cudaEventCreate(&e1));
   BC_CUDA(cudaEventCreate(&e2));
   BC_CUDA(cudaEventRecord(e0, st));
-  int64_t n_alive = 0, spills = 0;
+  int64_t n_alive = 0, n_heavy = 0, n_sub = 0;
   if (nloc > 0) {
     if (s.p_eff == 1) {
       p1_kernel<<<sms * 8, 256, 0, st>>>(P, s.aoff);
@@ -719,7 +1156,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
         copy_d2h(h, ctr.p, sizeof h, st);
         BC_CUDA(cudaStreamSynchronize(st));
         n_alive = (int64_t)h[CTR_ALIVE];
-        const int64_t max_need = (int64_t)h[CTR_MAXNEED];
+        const int64_t max_ro = (int64_t)h[CTR_MAXRO], max_scr = (int64_t)h[CTR_MAXSCR];
         if (n_alive > 0) {
           // pre-runtime LPT order: alive tasks by |C_L1|*|C_R1| descending
           DBuf<int32_t> ids, queue;
@@ -731,31 +1168,106 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           size_t tmp = 0;
           BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, cost.p, skeys.p, ids.p,
                                                             queue.p, nloc, 0, 32, st));
-          DBuf<char> t;
-          t.alloc(tmp, st);
-          BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, cost.p, skeys.p, ids.p,
-                                                            queue.p, nloc, 0, 32, st));
+          {
+            DBuf<char> t;
+            t.alloc(tmp, st);
+            BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, cost.p, skeys.p, ids.p,
+                                                              queue.p, nloc, 0, 32, st));
+          }
           launches += 2;
-          const int threads = 256, wpb = threads / 32;
-          const int budget = 2048;  // words of shared memory per warp
-          const size_t smem = (size_t)wpb * budget * 4;
-          auto kern = instr ? enum_kernel<true> : enum_kernel<false>;
+          const int wpb = ENUM_THREADS / 32;
+          const int budget = 2048;  // words of shared memory per warp for frames
+          const int map_w = (P.map_words + 1) / 2;
+          const size_t smem = (size_t)wpb * (budget + map_w) * 4;
+          const bool lazy = !has_rowL(s.p_eff, P.map_words) && s.p_eff == 4;
+          auto kern = instr ? (lazy ? enum_kernel<true, true> : enum_kernel<true, false>)
+                            : (lazy ? enum_kernel<false, true> : enum_kernel<false, false>);
           BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
           int per_sm = 0;
-          BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+          BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ENUM_THREADS, smem));
           if (per_sm < 1) per_sm = 1;
           const int64_t blocks = (int64_t)sms * per_sm;
-          DBuf<uint32_t> gs;
-          int64_t gs_words = 0;
-          if (max_need > budget) {
-            gs_words = (max_need + 31) & ~int64_t(31);
-            gs.alloc((size_t)blocks * wpb * gs_words, st);
+          const int64_t warps = blocks * wpb;
+          EnumArgs A{};
+          A.info = info.p;
+          A.queue = queue.p;
+          A.n_alive = n_alive;
+          A.budget_words = budget;
+          // heavy-task splitting (deep searches only): the LPT head
+          const int split_level = s.p_eff >= 6 ? 3 : 2;
+          if (allow_split && s.p_eff >= 5) n_heavy = std::min<int64_t>(n_alive, warps / 2);
+          DBuf<int64_t> hro, hsub, foff, soff;
+          DBuf<uint32_t> frames, sub_arena;
+          DBuf<unsigned long long> sub_index;
+          int64_t sub_words = 0, sub_cap = 0, heavy_scr = 0;
+          if (n_heavy > 0) {
+            hro.alloc(n_heavy + 1, st);
+            hsub.alloc(n_heavy + 1, st);
+            foff.alloc(n_heavy + 1, st);
+            hro.zero();
+            hsub.zero();
+            DBuf<unsigned long long> mscr;
+            mscr.alloc(1, st);
+            mscr.zero();
+            heavy_sizes<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(
+                info.p, queue.p, n_heavy, s.p_eff, instr, split_level, hro.p, hsub.p, mscr.p);
+            BC_CHECK_LAUNCH();
+            size_t t2 = 0;
+            BC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, hro.p, foff.p, n_heavy + 1, st));
+            DBuf<char> tb;
+            tb.alloc(t2, st);
+            BC_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, t2, hro.p, foff.p, n_heavy + 1, st));
+            int64_t frame_words = 0;
+            copy_d2h(&frame_words, foff.p + n_heavy, sizeof frame_words, st);
+            unsigned long long hs = 0;
+            copy_d2h(&hs, mscr.p, sizeof hs, st);
+            sub_words = sum_device(hsub.p, n_heavy, st);
+            heavy_scr = (int64_t)hs;
+            launches += 3;
+            sub_words = std::min<int64_t>(sub_words, int64_t(1) << 28);  // <= 1 GiB of records
+            sub_cap = std::max<int64_t>(1, sub_words / 5);
+            frames.alloc(frame_words, st);
+            sub_arena.alloc(sub_words, st);
+            sub_index.alloc(sub_cap, st);
+            A.frames = frames.p;
+            A.frame_off = foff.p;
+            A.sink.arena = sub_arena.p;
+            A.sink.arena_words = sub_words;
+            A.sink.index = sub_index.p;
+            A.sink.index_cap = sub_cap;
+            A.sink.level = split_level;
           }
-          kern<<<(unsigned)blocks, threads, smem, st>>>(P, info.p, queue.p, n_alive, budget,
-                                                       gs_words ? gs.p : nullptr, gs_words);
+          A.n_heavy = n_heavy;
+          DBuf<uint32_t> gs;
+          const int64_t need = std::max<int64_t>(max_ro + max_scr, heavy_scr);
+          if (need > budget) {
+            A.gscratch_words = (need + 31) & ~int64_t(31);
+            gs.alloc((size_t)warps * A.gscratch_words, st);
+            A.gscratch = gs.p;
+          }
+          kern<<<(unsigned)blocks, ENUM_THREADS, smem, st>>>(P, A);
           BC_CHECK_LAUNCH();
           launches++;
+          if (n_heavy > 0) {
+            unsigned long long hn = 0;
+            copy_d2h(&hn, ctr.p + CTR_SUB_N, sizeof hn, st);
+            BC_CUDA(cudaStreamSynchronize(st));
+            n_sub = std::min<int64_t>((int64_t)hn, sub_cap);
+            if (n_sub > 0) {
+              auto sk = instr ? sub_kernel<true> : sub_kernel<false>;
+              const size_t ssmem = (size_t)wpb * budget * 4;
+              BC_CUDA(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)ssmem));
+              int sper = 0;
+              BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sper, sk, ENUM_THREADS, ssmem));
+              if (sper < 1) sper = 1;
+              const int64_t sblocks = std::min<int64_t>((int64_t)sms * sper, blocks);
+              sk<<<(unsigned)sblocks, ENUM_THREADS, ssmem, st>>>(P, A, n_sub);
+              BC_CHECK_LAUNCH();
+              launches++;
+            }
+          }
         }
       }
     }
@@ -768,8 +1280,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   copy_d2h(h_acc, acc.p, sizeof h_acc, st);
   copy_d2h(h_ctr, ctr.p, sizeof h_ctr, st);
   copy_d2h(&h_ovf, ovf.p, sizeof h_ovf, st);
-  if (want_tc)
-    copy_d2h(cfg.task_counts, tcounts.p, 2 * n_tasks * sizeof(uint64_t), st);
+  if (want_tc) copy_d2h(cfg.task_counts, tcounts.p, 2 * n_tasks * sizeof(uint64_t), st);
   BC_CUDA(cudaStreamSynchronize(st));
   float t1 = 0, t2 = 0;
   BC_CUDA(cudaEventElapsedTime(&t1, e0, e1));
@@ -778,13 +1289,12 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
   if (h_ovf == 2) throw Error(BC_ECUDA, "enumeration frame exceeded its scratch sizing");
-  spills = (int64_t)h_ctr[CTR_SPILL];
-  (void)spills;
   out.count_lo = h_acc[0];
   out.count_hi = h_acc[1];
   out.overflow = h_ovf ? 1 : 0;
   out.tasks_consumed = nloc;
   out.tasks_alive = n_alive;
+  out.tasks_split = n_heavy;
   out.tasks_stolen = (int64_t)h_ctr[CTR_STOLEN];
   out.batches_executed = (s.p_eff >= 2 ? nloc : 0) + (int64_t)h_ctr[CTR_BATCHES];
   out.intersections = (int64_t)h_ctr[CTR_INTER];
@@ -793,6 +1303,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   out.time_level1 = t1 * 1e-3;
   out.time_enum = t2 * 1e-3;
   out.kernel_launches += launches;
+  (void)n_sub;
 }
 
 }  // namespace bc
