@@ -114,6 +114,15 @@ int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
     bc::DevGraph &g = h->g;
     g.device = device;
     BC_CUDA(cudaSetDevice(device));
+    {
+      // keep freed stream-ordered allocations cached in the pool: the default
+      // release threshold (0) hands memory back at every synchronisation and
+      // turns the next call's scratch allocations into driver remaps
+      cudaMemPool_t pool;
+      BC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = UINT64_MAX;
+      BC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     BC_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
     g.n_u = n_u;
     g.n_v = n_v;

@@ -234,9 +234,15 @@ __host__ __device__ __forceinline__ int64_t ro_words(int nR, int nL, int wR, int
   return (w + 3) & ~int64_t(3);
 }
 
+// DFS stack: nodes at levels 1 .. p_eff-3 are expanded warp-cooperatively
+// (leaf-parents at p_eff-2 are finished lane-parallel without a frame).
+__host__ __device__ __forceinline__ int stack_levels(int p_eff) {
+  return p_eff - 3 > 1 ? p_eff - 3 : 1;
+}
+
 __host__ __device__ __forceinline__ int64_t scratch_words(int nR, int nL, int p_eff) {
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
-  const int64_t levels = p_eff - 2;
+  const int64_t levels = stack_levels(p_eff);
   return ((int64_t)nL + levels * (WR + WL + nL + 2) + 3) & ~int64_t(3);
 }
 
@@ -256,7 +262,7 @@ __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d, b
 }
 
 __device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims &d, int p_eff) {
-  const int levels = p_eff - 2;
+  const int levels = stack_levels(p_eff);
   f.cand = (int *)p; p += d.nL;
   f.setR = p; p += (int64_t)levels * d.WR;
   f.setL = p; p += (int64_t)levels * d.WL;
@@ -848,14 +854,14 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
 struct EnumArgs {
   const Info *__restrict__ info;
   const int32_t *__restrict__ queue;  // local task ids, LPT order
-  int64_t n_alive;
-  int64_t n_heavy;                    // queue[0, n_heavy) are split
+  int64_t q0, q1;                     // this launch drains queue[q0, q1)
   int budget_words;                   // shared memory per warp for frames
   uint32_t *gscratch;                 // per-warp global fallback
   int64_t gscratch_words;
-  uint32_t *frames;                   // heavy read-only frames
-  const int64_t *frame_off;           // [n_heavy]
+  uint32_t *frames;                   // SPLIT: read-only frames of queue[q0, q1)
+  const int64_t *frame_off;           // SPLIT: [q1 - q0]
   SplitSink sink;
+  const unsigned long long *sub_order;  // sub_kernel: record offsets, LPT order
 };
 
 __device__ __forceinline__ void finish_task(const Params &P, Acc128 acc, int64_t t, bool atomic,
@@ -897,7 +903,10 @@ __device__ __forceinline__ void flush_tallies(const Params &P, const Acc128 &tot
 
 constexpr int ENUM_THREADS = 256;
 
-template <bool INSTR, bool LAZY>
+// Whole tasks (SPLIT = false) or the top levels of every task with its frame
+// written to the global frame arena and split-level nodes pushed as sub-tasks
+// (SPLIT = true, p_eff >= 5).
+template <bool INSTR, bool LAZY, bool SPLIT>
 __global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArgs A) {
   extern __shared__ uint32_t smem[];
   const int lane = lane_id();
@@ -918,21 +927,19 @@ __global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArg
   for (;;) {
     long long qi = 0;
     if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
-    qi = __shfl_sync(FULL, qi, 0);
-    if (qi >= A.n_alive) break;
+    qi = __shfl_sync(FULL, qi, 0) + A.q0;
+    if (qi >= A.q1) break;
     claims++;
     const int j = A.queue[qi];
     const int64_t t = P.shard + (int64_t)j * P.nshards;
     const int2 tk = P.tasks[t];
     const Dims d = dims_of(A.info[j]);
-    const bool heavy = qi < A.n_heavy;
-    const bool rowL = heavy || has_rowL(p_eff, P.map_words);
+    const bool rowL = SPLIT || has_rowL(p_eff, P.map_words);
     const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, rowL, INSTR);
     const int64_t sc = scratch_words(d.nR, d.nL, p_eff);
-    Frame f;
     uint32_t *ro_base, *sc_base;
-    if (heavy) {
-      ro_base = A.frames + A.frame_off[qi];
+    if (SPLIT) {
+      ro_base = A.frames + A.frame_off[qi - A.q0];
       if (sc <= A.budget_words) sc_base = my_smem;
       else { sc_base = my_global; spills++; }
     } else if (ro + sc <= A.budget_words) {
@@ -943,30 +950,31 @@ __global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArg
       sc_base = my_global + ro;
       spills++;
     }
-    if (!sc_base || (sc_base == my_global && (heavy ? sc : ro + sc) > A.gscratch_words)) {
+    if (!sc_base || (sc_base == my_global && (SPLIT ? sc : ro + sc) > A.gscratch_words)) {
       if (lane == 0) atomicExch(P.overflow, 2);  // cannot happen: sized from level-1 maxima
       continue;
     }
+    Frame f;
     carve_ro(f, ro_base, d, rowL, INSTR);
     carve_scratch(f, sc_base, d, p_eff);
     build_frame<INSTR, LAZY>(P, f, d, tk.x, tk.y, map);
     init_root_sets(f, d);
     Acc128 acc{0, 0};
-    if (heavy) {
+    if (SPLIT) {
       SplitSink sink = A.sink;
-      sink.frame_off = A.frame_off[qi];
+      sink.frame_off = A.frame_off[qi - A.q0];
       sink.task_j = j;
       dfs<INSTR, false>(P, f, d, 1, map, acc, tl, &sink);
     } else {
       dfs<INSTR, LAZY>(P, f, d, 1, map, acc, tl, nullptr);
     }
     clear_map(map, f, d);
-    finish_task(P, acc, t, heavy, total);
+    finish_task(P, acc, t, SPLIT, total);
   }
   flush_tallies(P, total, tl, claims, spills, INSTR);
 }
 
-// Split nodes of heavy tasks: warp per sub-task record.
+// Split nodes: warp per sub-task record, records in LPT order.
 template <bool INSTR>
 __global__ void __launch_bounds__(ENUM_THREADS, 2) sub_kernel(Params P, EnumArgs A, int64_t n_sub) {
   extern __shared__ uint32_t smem[];
@@ -984,7 +992,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, 2) sub_kernel(Params P, EnumArgs
     if (lane == 0) k = (long long)atomicAdd(P.ctr + CTR_SUB_NEXT, 1ull);
     k = __shfl_sync(FULL, k, 0);
     if (k >= n_sub) break;
-    const uint32_t *rec = A.sink.arena + A.sink.index[k];
+    const uint32_t *rec = A.sink.arena + A.sub_order[k];
     const int j = (int)rec[0];
     const int lv = (int)rec[1];
     const int64_t foff = (int64_t)rec[2] | ((int64_t)rec[3] << 32);
@@ -1015,18 +1023,32 @@ __global__ void iota32(int32_t *a, int64_t n) {
   if (i < n) a[i] = (int32_t)i;
 }
 
-// frame / sub-task sizing for the heavy head of the queue
-__global__ void heavy_sizes(const Info *info, const int32_t *queue, int64_t n_heavy, int p_eff,
-                            bool instr, int split_level, int64_t *ro, int64_t *sub,
-                            unsigned long long *max_scr) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_heavy) return;
-  const Info in = info[queue[i]];
+// frame / sub-task arena sizes for queue[q0, q1)
+__global__ void split_sizes(const Info *info, const int32_t *queue, int64_t q0, int64_t q1,
+                            bool instr, int split_level, int64_t *ro, int64_t *sub) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= q1 - q0) return;
+  const Info in = info[queue[q0 + i]];
   ro[i] = ro_words(in.cr, in.cl, in.wr, in.wl, true, instr);
   const int64_t WR = (in.cr + 31) / 32, WL = (in.cl + 31) / 32;
   const int64_t nodes = split_level == 2 ? in.cl : (int64_t)in.cl * (in.cl - 1) / 2;
   sub[i] = nodes * (4 + WR + WL);
-  atomicMax(max_scr, (unsigned long long)scratch_words(in.cr, in.cl, p_eff));
+}
+
+// sub-task LPT key: candidates left below the node, |L| * |R| (saturating)
+__global__ void sub_keys(const uint32_t *arena, const unsigned long long *index, int64_t n,
+                         const Info *info, uint32_t *key, unsigned long long *val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t *rec = arena + index[i];
+  const Info in = info[rec[0]];
+  const int WR = (in.cr + 31) >> 5, WL = (in.cl + 31) >> 5;
+  unsigned cr = 0, cl = 0;
+  for (int w = 0; w < WR; w++) cr += __popc(rec[4 + w]);
+  for (int w = 0; w < WL; w++) cl += __popc(rec[4 + WR + w]);
+  const unsigned long long k = (unsigned long long)cl * cl * (cr ? cr : 1);
+  key[i] = k > 0xffffffffull ? 0xffffffffu : (uint32_t)k;
+  val[i] = index[i];
 }
 
 // C(c, q) for c <= max_deg as exact u128; returns first c whose value needs > 128 bits.
@@ -1066,6 +1088,34 @@ T sum_device(const T *p, int64_t n, cudaStream_t st) {
   copy_d2h(&h, out.p, sizeof(T), st);
   BC_CUDA(cudaStreamSynchronize(st));
   return h;
+}
+
+template <typename K, typename V>
+void sort_pairs_desc(const K *kin, K *kout, const V *vin, V *vout, int64_t n, cudaStream_t st) {
+  size_t tmp = 0;
+  BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, kin, kout, vin, vout, n, 0,
+                                                    (int)sizeof(K) * 8, st));
+  DBuf<char> t;
+  t.alloc(tmp, st);
+  BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, kin, kout, vin, vout, n, 0,
+                                                    (int)sizeof(K) * 8, st));
+}
+
+template <typename T>
+void scan_excl(const T *in, T *out, int64_t n, cudaStream_t st) {
+  size_t tmp = 0;
+  BC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
+  DBuf<char> t;
+  t.alloc(tmp, st);
+  BC_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, st));
+}
+
+template <typename KERN>
+int blocks_per_sm(KERN kern, size_t smem) {
+  BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ENUM_THREADS, smem));
+  return per_sm < 1 ? 1 : per_sm;
 }
 
 }  // namespace
@@ -1124,150 +1174,179 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   // slot map over anchor words for rowL (u16 per word) when it is small
   const int64_t anchor_words = (s.n + 31) / 32;
   P.map_words = (s.p_eff >= 4 && anchor_words <= 4096) ? (int)((anchor_words + 1) & ~1) : 0;
+  const int map_w = (P.map_words + 1) / 2;
+  const int wpb = ENUM_THREADS / 32;
 
   cudaEvent_t e0, e1, e2;
   BC_CUDA(cudaEventCreate(&e0));
   BC_CUDA(cudaEventCreate(&e1));
   BC_CUDA(cudaEventCreate(&e2));
   BC_CUDA(cudaEventRecord(e0, st));
-  int64_t n_alive = 0, n_heavy = 0, n_sub = 0;
-  if (nloc > 0) {
-    if (s.p_eff == 1) {
-      p1_kernel<<<sms * 8, 256, 0, st>>>(P, s.aoff);
+  int64_t n_alive = 0, n_split = 0, n_sub_total = 0;
+  if (nloc > 0 && s.p_eff == 1) {
+    p1_kernel<<<sms * 8, 256, 0, st>>>(P, s.aoff);
+    BC_CHECK_LAUNCH();
+    launches++;
+    BC_CUDA(cudaEventRecord(e1, st));
+  } else if (nloc > 0) {
+    DBuf<Info> info;
+    DBuf<uint32_t> cost;
+    info.alloc(nloc, st);
+    cost.alloc(nloc, st);
+    {
+      int64_t blocks = (nloc * 32 + 255) / 256;
+      blocks = std::min<int64_t>(blocks, (int64_t)sms * 32);
+      if (instr) level1_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
+      else level1_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
       BC_CHECK_LAUNCH();
       launches++;
-      BC_CUDA(cudaEventRecord(e1, st));
-    } else {
-      DBuf<Info> info;
-      DBuf<uint32_t> cost;
-      info.alloc(nloc, st);
-      cost.alloc(nloc, st);
-      {
-        int64_t blocks = (nloc * 32 + 255) / 256;
-        blocks = std::min<int64_t>(blocks, (int64_t)sms * 32);
-        if (instr) level1_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
-        else level1_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
-        BC_CHECK_LAUNCH();
-        launches++;
-      }
-      BC_CUDA(cudaEventRecord(e1, st));
-      if (s.p_eff >= 3) {
-        unsigned long long h[CTR_COUNT];
-        copy_d2h(h, ctr.p, sizeof h, st);
-        BC_CUDA(cudaStreamSynchronize(st));
-        n_alive = (int64_t)h[CTR_ALIVE];
-        const int64_t max_ro = (int64_t)h[CTR_MAXRO], max_scr = (int64_t)h[CTR_MAXSCR];
-        if (n_alive > 0) {
-          // pre-runtime LPT order: alive tasks by |C_L1|*|C_R1| descending
-          DBuf<int32_t> ids, queue;
-          DBuf<uint32_t> skeys;
-          ids.alloc(nloc, st);
-          queue.alloc(nloc, st);
-          skeys.alloc(nloc, st);
-          iota32<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(ids.p, nloc);
-          size_t tmp = 0;
-          BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, cost.p, skeys.p, ids.p,
-                                                            queue.p, nloc, 0, 32, st));
-          {
-            DBuf<char> t;
-            t.alloc(tmp, st);
-            BC_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, cost.p, skeys.p, ids.p,
-                                                              queue.p, nloc, 0, 32, st));
-          }
-          launches += 2;
-          const int wpb = ENUM_THREADS / 32;
-          const int budget = 2048;  // words of shared memory per warp for frames
-          const int map_w = (P.map_words + 1) / 2;
+    }
+    BC_CUDA(cudaEventRecord(e1, st));
+    if (s.p_eff >= 3) {
+      unsigned long long h[CTR_COUNT];
+      copy_d2h(h, ctr.p, sizeof h, st);
+      BC_CUDA(cudaStreamSynchronize(st));
+      n_alive = (int64_t)h[CTR_ALIVE];
+      const int64_t max_ro = (int64_t)h[CTR_MAXRO], max_scr = (int64_t)h[CTR_MAXSCR];
+      if (n_alive > 0) {
+        // pre-runtime LPT order: alive tasks by |C_L1|*|C_R1| descending
+        DBuf<int32_t> ids, queue;
+        DBuf<uint32_t> skeys;
+        ids.alloc(nloc, st);
+        queue.alloc(nloc, st);
+        skeys.alloc(nloc, st);
+        iota32<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(ids.p, nloc);
+        sort_pairs_desc(cost.p, skeys.p, ids.p, queue.p, nloc, st);
+        launches += 2;
+        EnumArgs A{};
+        A.info = info.p;
+        A.queue = queue.p;
+        const bool split = allow_split && s.p_eff >= 5;
+        if (!split) {
+          // whole tasks per warp; frames in shared memory
+          const bool lazy = s.p_eff == 4 && !has_rowL(s.p_eff, P.map_words);
+          const int budget = 2048;
           const size_t smem = (size_t)wpb * (budget + map_w) * 4;
-          const bool lazy = !has_rowL(s.p_eff, P.map_words) && s.p_eff == 4;
-          auto kern = instr ? (lazy ? enum_kernel<true, true> : enum_kernel<true, false>)
-                            : (lazy ? enum_kernel<false, true> : enum_kernel<false, false>);
-          BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-          int per_sm = 0;
-          BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ENUM_THREADS, smem));
-          if (per_sm < 1) per_sm = 1;
-          const int64_t blocks = (int64_t)sms * per_sm;
-          const int64_t warps = blocks * wpb;
-          EnumArgs A{};
-          A.info = info.p;
-          A.queue = queue.p;
-          A.n_alive = n_alive;
+          auto kern = instr ? (lazy ? enum_kernel<true, true, false> : enum_kernel<true, false, false>)
+                            : (lazy ? enum_kernel<false, true, false> : enum_kernel<false, false, false>);
+          const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
+          A.q0 = 0;
+          A.q1 = n_alive;
           A.budget_words = budget;
-          // heavy-task splitting (deep searches only): the LPT head
-          const int split_level = s.p_eff >= 6 ? 3 : 2;
-          if (allow_split && s.p_eff >= 5) n_heavy = std::min<int64_t>(n_alive, warps / 2);
-          DBuf<int64_t> hro, hsub, foff, soff;
-          DBuf<uint32_t> frames, sub_arena;
-          DBuf<unsigned long long> sub_index;
-          int64_t sub_words = 0, sub_cap = 0, heavy_scr = 0;
-          if (n_heavy > 0) {
-            hro.alloc(n_heavy + 1, st);
-            hsub.alloc(n_heavy + 1, st);
-            foff.alloc(n_heavy + 1, st);
-            hro.zero();
-            hsub.zero();
-            DBuf<unsigned long long> mscr;
-            mscr.alloc(1, st);
-            mscr.zero();
-            heavy_sizes<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(
-                info.p, queue.p, n_heavy, s.p_eff, instr, split_level, hro.p, hsub.p, mscr.p);
-            BC_CHECK_LAUNCH();
-            size_t t2 = 0;
-            BC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, hro.p, foff.p, n_heavy + 1, st));
-            DBuf<char> tb;
-            tb.alloc(t2, st);
-            BC_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, t2, hro.p, foff.p, n_heavy + 1, st));
-            int64_t frame_words = 0;
-            copy_d2h(&frame_words, foff.p + n_heavy, sizeof frame_words, st);
-            unsigned long long hs = 0;
-            copy_d2h(&hs, mscr.p, sizeof hs, st);
-            sub_words = sum_device(hsub.p, n_heavy, st);
-            heavy_scr = (int64_t)hs;
-            launches += 3;
-            sub_words = std::min<int64_t>(sub_words, int64_t(1) << 28);  // <= 1 GiB of records
-            sub_cap = std::max<int64_t>(1, sub_words / 5);
-            frames.alloc(frame_words, st);
-            sub_arena.alloc(sub_words, st);
-            sub_index.alloc(sub_cap, st);
-            A.frames = frames.p;
-            A.frame_off = foff.p;
-            A.sink.arena = sub_arena.p;
-            A.sink.arena_words = sub_words;
-            A.sink.index = sub_index.p;
-            A.sink.index_cap = sub_cap;
-            A.sink.level = split_level;
-          }
-          A.n_heavy = n_heavy;
           DBuf<uint32_t> gs;
-          const int64_t need = std::max<int64_t>(max_ro + max_scr, heavy_scr);
-          if (need > budget) {
-            A.gscratch_words = (need + 31) & ~int64_t(31);
-            gs.alloc((size_t)warps * A.gscratch_words, st);
+          if (max_ro + max_scr > budget) {
+            A.gscratch_words = (max_ro + max_scr + 31) & ~int64_t(31);
+            gs.alloc((size_t)blocks * wpb * A.gscratch_words, st);
             A.gscratch = gs.p;
           }
           kern<<<(unsigned)blocks, ENUM_THREADS, smem, st>>>(P, A);
           BC_CHECK_LAUNCH();
           launches++;
-          if (n_heavy > 0) {
+        } else {
+          // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
+          // writes every frame to the frame arena and pushes the split-level nodes,
+          // then sub_kernel drains them heaviest first with every warp.
+          const int split_level = s.p_eff <= 6 ? 2 : 3;
+          const int budget = 1024;
+          const size_t smem = (size_t)wpb * (budget + map_w) * 4;
+          auto kern = instr ? enum_kernel<true, false, true> : enum_kernel<false, false, true>;
+          auto sk = instr ? sub_kernel<true> : sub_kernel<false>;
+          const size_t ssmem = (size_t)wpb * budget * 4;
+          const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
+          const int64_t sblocks = std::min<int64_t>((int64_t)sms * blocks_per_sm(sk, ssmem), blocks);
+          A.budget_words = budget;
+          DBuf<uint32_t> gs;
+          if (max_scr > budget) {
+            A.gscratch_words = (max_scr + 31) & ~int64_t(31);
+            gs.alloc((size_t)blocks * wpb * A.gscratch_words, st);
+            A.gscratch = gs.p;
+          }
+          const int64_t arena_limit = int64_t(1) << 28;  // words per arena (1 GiB)
+          DBuf<int64_t> ro, sub, foff, soff;
+          ro.alloc(n_alive + 1, st);
+          sub.alloc(n_alive + 1, st);
+          foff.alloc(n_alive + 1, st);
+          soff.alloc(n_alive + 1, st);
+          ro.zero();
+          sub.zero();
+          split_sizes<<<(unsigned)((n_alive + 255) / 256), 256, 0, st>>>(
+              info.p, queue.p, 0, n_alive, instr, split_level, ro.p, sub.p);
+          scan_excl(ro.p, foff.p, n_alive + 1, st);
+          scan_excl(sub.p, soff.p, n_alive + 1, st);
+          std::vector<int64_t> hf(n_alive + 1), hs(n_alive + 1);
+          copy_d2h(hf.data(), foff.p, (n_alive + 1) * 8, st);
+          copy_d2h(hs.data(), soff.p, (n_alive + 1) * 8, st);
+          BC_CUDA(cudaStreamSynchronize(st));
+          launches += 3;
+          int64_t q0 = 0;
+          while (q0 < n_alive) {
+            // grow the chunk while both arenas stay under the limit
+            int64_t q1 = q0 + 1;
+            {
+              int64_t lo = q0 + 1, hi = n_alive;
+              while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) / 2;
+                if (hf[mid] - hf[q0] <= arena_limit && hs[mid] - hs[q0] <= arena_limit) lo = mid;
+                else hi = mid - 1;
+              }
+              q1 = lo;
+            }
+            const int64_t fw = hf[q1] - hf[q0];
+            const int64_t sw = std::max<int64_t>(hs[q1] - hs[q0], 8);
+            DBuf<uint32_t> frames, arena;
+            DBuf<unsigned long long> index;
+            DBuf<int64_t> local_off;
+            frames.alloc(fw, st);
+            arena.alloc(sw, st);
+            const int64_t cap = sw / 6 + 1;
+            index.alloc(cap, st);
+            local_off.alloc(q1 - q0, st);
+            // frame offsets relative to the chunk
+            {
+              std::vector<int64_t> lo_off(q1 - q0);
+              for (int64_t i = q0; i < q1; i++) lo_off[i - q0] = hf[i] - hf[q0];
+              copy_h2d(local_off.p, lo_off.data(), (q1 - q0) * 8, st);
+            }
+            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
+            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_USED, 0, 8, st));
+            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_N, 0, 8, st));
+            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_NEXT, 0, 8, st));
+            A.q0 = q0;
+            A.q1 = q1;
+            A.frames = frames.p;
+            A.frame_off = local_off.p;
+            A.sink.arena = arena.p;
+            A.sink.arena_words = sw;
+            A.sink.index = index.p;
+            A.sink.index_cap = cap;
+            A.sink.level = split_level;
+            kern<<<(unsigned)blocks, ENUM_THREADS, smem, st>>>(P, A);
+            BC_CHECK_LAUNCH();
             unsigned long long hn = 0;
             copy_d2h(&hn, ctr.p + CTR_SUB_N, sizeof hn, st);
             BC_CUDA(cudaStreamSynchronize(st));
-            n_sub = std::min<int64_t>((int64_t)hn, sub_cap);
+            const int64_t n_sub = std::min<int64_t>((int64_t)hn, cap);
+            launches += 1;
             if (n_sub > 0) {
-              auto sk = instr ? sub_kernel<true> : sub_kernel<false>;
-              const size_t ssmem = (size_t)wpb * budget * 4;
-              BC_CUDA(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)ssmem));
-              int sper = 0;
-              BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sper, sk, ENUM_THREADS, ssmem));
-              if (sper < 1) sper = 1;
-              const int64_t sblocks = std::min<int64_t>((int64_t)sms * sper, blocks);
+              DBuf<uint32_t> k0, k1;
+              DBuf<unsigned long long> v1;
+              k0.alloc(n_sub, st);
+              k1.alloc(n_sub, st);
+              DBuf<unsigned long long> v0;
+              v0.alloc(n_sub, st);
+              v1.alloc(n_sub, st);
+              sub_keys<<<(unsigned)((n_sub + 255) / 256), 256, 0, st>>>(arena.p, index.p, n_sub,
+                                                                      info.p, k0.p, v0.p);
+              sort_pairs_desc(k0.p, k1.p, v0.p, v1.p, n_sub, st);
+              A.sub_order = v1.p;
               sk<<<(unsigned)sblocks, ENUM_THREADS, ssmem, st>>>(P, A, n_sub);
               BC_CHECK_LAUNCH();
-              launches++;
+              launches += 3;
             }
+            n_sub_total += n_sub;
+            q0 = q1;
           }
+          n_split = n_alive;
         }
       }
     }
@@ -1294,7 +1373,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   out.overflow = h_ovf ? 1 : 0;
   out.tasks_consumed = nloc;
   out.tasks_alive = n_alive;
-  out.tasks_split = n_heavy;
+  out.tasks_split = n_split;
   out.tasks_stolen = (int64_t)h_ctr[CTR_STOLEN];
   out.batches_executed = (s.p_eff >= 2 ? nloc : 0) + (int64_t)h_ctr[CTR_BATCHES];
   out.intersections = (int64_t)h_ctr[CTR_INTER];
@@ -1303,7 +1382,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   out.time_level1 = t1 * 1e-3;
   out.time_enum = t2 * 1e-3;
   out.kernel_launches += launches;
-  (void)n_sub;
+  (void)n_sub_total;
 }
 
 }  // namespace bc
