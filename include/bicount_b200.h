@@ -141,6 +141,11 @@ void bc_structs_destroy(bc_structs *s);
 /* Drop cached device state (streams, scratch). */
 void bc_shutdown(void);
 
+/* Development builds compiled with -DBC_PHASE_PROF: per-phase SM-cycle tallies of
+ * the enumeration since the last read (reset on read); returns the number of
+ * phases written, 0 in normal builds (out is zero-filled). */
+int bc_debug_phase_cycles(uint64_t *out, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

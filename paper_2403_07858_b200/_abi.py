@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbicount_b200.so")
+# BC_LIB selects a development build (e.g. the phase-profiling one); default in-tree .so
+LIB_PATH = os.environ.get("BC_LIB") or os.path.join(HERE, "libbicount_b200.so")
 
 BC_OK, BC_EINVAL, BC_ECUDA, BC_ENCCL, BC_EOOM, BC_EOVERFLOW = 0, -1, -2, -3, -4, -5
 BC_FLAG_TASK_COUNTS, BC_FLAG_INSTRUMENT, BC_FLAG_NO_SPLIT = 1, 2, 4
@@ -22,7 +23,7 @@ BC_FLAG_TASK_COUNTS, BC_FLAG_INSTRUMENT, BC_FLAG_NO_SPLIT = 1, 2, 4
 # every symbol include/bicount_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("bc_abi_version", "bc_last_error", "bc_device_count", "bc_count", "bc_graph_create",
             "bc_graph_count", "bc_graph_destroy", "bc_prepare", "bc_export_len", "bc_export",
-            "bc_structs_destroy", "bc_shutdown")
+            "bc_structs_destroy", "bc_shutdown", "bc_debug_phase_cycles")
 
 
 class BcConfig(C.Structure):
@@ -85,6 +86,8 @@ def _declare(L):
     L.bc_structs_destroy.argtypes = [vp]
     L.bc_shutdown.restype = None
     L.bc_shutdown.argtypes = []
+    L.bc_debug_phase_cycles.restype = C.c_int
+    L.bc_debug_phase_cycles.argtypes = [vp, i32]
 
 
 def open_library():

@@ -42,11 +42,13 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          out: str | None = None) -> str:
+    lib = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-           "--expt-relaxed-constexpr", "-shared", "-o", LIB + ".tmp", *sources(),
+           "--expt-relaxed-constexpr", "-shared", "-o", lib + ".tmp", *sources(),
            "-lcudart"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -58,10 +60,19 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         raise RuntimeError("nvcc build of libbicount_b200.so failed")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:  # development variants: --variant NAME -DX=Y ...
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]
+        print(build(force=True, verbose="-v" in sys.argv, extra=defs,
+                    out=os.path.join(HERE, f"libbicount_b200_{name}.so")))
+    elif "--prof" in sys.argv:  # phase-profiling development build (BC_LIB=... to load it)
+        print(build(force=True, verbose="-v" in sys.argv, extra=["-DBC_PHASE_PROF"],
+                    out=os.path.join(HERE, "libbicount_b200_prof.so")))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

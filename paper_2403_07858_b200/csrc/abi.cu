@@ -352,4 +352,12 @@ void bc_structs_destroy(bc_structs *r) {
 
 void bc_shutdown(void) {}
 
+int bc_debug_phase_cycles(uint64_t *out, int32_t n) {
+  try {
+    return (int)bc::debug_phase_cycles(out, n);
+  } catch (const bc::Error &err) {
+    return fail(err.code, err.what());
+  }
+}
+
 }  // extern "C"

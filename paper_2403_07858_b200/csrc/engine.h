@@ -107,4 +107,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out);
 
 int num_sms(int device);
 
+// BC_PHASE_PROF builds: per-phase SM cycles of the last enumeration (reset on read).
+int64_t debug_phase_cycles(uint64_t *out, int n);
+
 }  // namespace bc

@@ -11,6 +11,9 @@
 // Every array is bit-identical to the reference's (tests/test_gpu_parity.py).
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+#include <ctime>
+
 #include "engine.h"
 
 namespace bc {
@@ -431,9 +434,30 @@ int num_sms(int device) {
   return v;
 }
 
+// BC_DEBUG=1: per-stage wall time of the preprocessing on stderr (development).
+struct StageTimer {
+  bool on;
+  cudaStream_t st;
+  double t0;
+  explicit StageTimer(cudaStream_t s) : on(getenv("BC_DEBUG") != nullptr), st(s), t0(now()) {}
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+  }
+  void mark(const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const double t = now();
+    fprintf(stderr, "[bc prep] %-10s %8.3f ms\n", what, 1e3 * (t - t0));
+    t0 = t;
+  }
+};
+
 void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s) {
   if (p < 1 || q < 1) throw Error(BC_EINVAL, "p and q must be >= 1");
   cudaStream_t st = g.stream;
+  StageTimer tm(st);
   s.stream = st;
   const int sms = num_sms(g.device);
   int64_t &L = s.launches;
@@ -534,6 +558,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     ntiles = 1;
   }
 
+  tm.mark("2-hop");
   // ---- priority (graph.py:227-243) or rank override (engine.py:130-134) ----
   s.rank.alloc(n ? n : 1, st);
   s.order.alloc(n ? n : 1, st);
@@ -573,6 +598,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     }
   }
 
+  tm.mark("priority");
   // ---- directed 2-hop lists (graph.py:218-224) ----
   {
     DBuf<int64_t> dsize;
@@ -591,12 +617,14 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
           s.dir_idx.p);
     L += 3;
   }
+  tm.mark("directed");
   // ---- HTB encodings (htb.py:104-115) ----
   build_htb(s.aoff, s.aidx, n, s.hadj_off, s.hadj_idx, s.hadj_val, s.adj_words, s.max_adj_slice,
             sms, st, L);
   build_htb(s.dir_off.p, s.dir_idx.p, n, s.hdir_off, s.hdir_idx, s.hdir_val, s.dir2_words,
             s.max_dir_slice, sms, st, L);
 
+  tm.mark("htb");
   // ---- dense bitmaps of the longest adjacency rows (probe = one load) ----
   s.dense_id.alloc(n ? n : 1, st);
   BC_CUDA(cudaMemsetAsync(s.dense_id.p, 0xff, (n ? n : 1) * sizeof(int32_t), st));
@@ -638,6 +666,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     }
   }
 
+  tm.mark("dense");
   // ---- tasks (engine.py:147-173) ----
   {
     DBuf<uint8_t> mask;
@@ -672,6 +701,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
                                                       s.dir_idx.p, n, s.p_eff, s.tasks.p);
     L += 3;
   }
+  tm.mark("tasks");
   (void)p;
 }
 

@@ -38,11 +38,64 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.h"
 
 namespace bc {
+
+// Per-phase SM-cycle tallies (lane 0 of every warp) in -DBC_PHASE_PROF builds:
+// 0 claim, 1 level-1 re-materialisation, 2 decode + slot map, 3 rows,
+// 4 expansions, 5 leaf-parents, 6 finish.
+#ifdef BC_PHASE_PROF
+__device__ unsigned long long g_phase[16];
+__device__ __forceinline__ long long clk() {
+  long long c = 0;
+#ifdef __CUDA_ARCH__
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+#endif
+  return c;
+}
+struct PhaseClock {
+  unsigned long long t[8];
+  long long last;
+  __device__ __forceinline__ PhaseClock() : last(clk()) {
+    for (int i = 0; i < 8; i++) t[i] = 0;
+  }
+  __device__ __forceinline__ void mark(int i) {
+    const long long n = clk();
+    t[i] += (unsigned long long)(n - last);
+    last = n;
+  }
+  __device__ __forceinline__ void flush() {
+    if ((threadIdx.x & 31) == 0)
+      for (int i = 0; i < 8; i++) atomicAdd(&g_phase[i], t[i]);
+  }
+};
+#else
+struct PhaseClock {
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush() {}
+};
+#endif
+#define PH_DECL PhaseClock ph_;
+#define PH_MARK(i) ph_.mark(i)
+#define PH_FLUSH() ph_.flush()
+
+int64_t debug_phase_cycles(uint64_t *out, int n) {
+#ifdef BC_PHASE_PROF
+  unsigned long long h[16];
+  BC_CUDA(cudaMemcpyFromSymbol(h, g_phase, sizeof h));
+  for (int i = 0; i < n && i < 16; i++) out[i] = h[i];
+  const unsigned long long z[16] = {0};
+  BC_CUDA(cudaMemcpyToSymbol(g_phase, z, sizeof z));
+  return 16;
+#else
+  for (int i = 0; i < n; i++) out[i] = 0;
+  return 0;
+#endif
+}
 
 namespace {
 
@@ -464,78 +517,185 @@ __device__ __forceinline__ unsigned node_batches(const Params &P, unsigned ncand
                                                  bool leaf) {
   if (!ncand) return 0;
   if (P.mode_dfs) return ncand;
-  unsigned b = (unsigned)P.cap / (unsigned)(wr > 1 ? wr : 1);
-  if (!leaf) {
-    const unsigned b2 = (unsigned)P.cap / (unsigned)(wl > 1 ? wl : 1);
-    if (b2 < b) b = b2;
-  }
+  const unsigned cap = (unsigned)P.cap;
+  const unsigned w = (unsigned)(wr > 1 ? wr : 1), w2 = leaf ? 1u : (unsigned)(wl > 1 ? wl : 1);
+  const unsigned wm = w > w2 ? w : w2;  // b = cap / max(wr, wl)
+  if ((unsigned long long)ncand * wm <= cap) return 1;  // one batch: no division
+  unsigned b = cap / wm;
   if (b < 1) b = 1;
   return (ncand + b - 1) / b;
 }
 
-// Leaf-parent nodes, one per lane.  Node u (a survivor of the node at
-// `level`) has R' = R & rowR[u] and L' = L & rowL[u] -- or, with LAZY
-// (p_eff = 4, level 1), L' = dir2(u) & C_L1 walked through the slot map --
-// and its children are leaves: add C(|R' & rowR[w]|, q) for w in L'
-// (engine.py:342-347).  No warp synchronisation inside.
-template <bool INSTR, bool LAZY>
-__device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, const Dims &d,
-                                             int level, const int *list, int n,
-                                             const uint16_t *map, Acc128 &acc, Tally &tl) {
-  const int lane = lane_id();
-  const int WR = d.WR, WL = d.WL;
-  const uint32_t *R = f.setR + (level - 1) * WR;
-  const uint32_t *Ls = f.setL + (level - 1) * WL;
-  const int q = P.q_eff;
-  for (int i = lane; i < n; i += 32) {
-    const int u = list[i];
-    const uint32_t *ru = f.rowR + (int64_t)u * WR;
-    const int wr = lane_words(R, ru, f.r_pre, d.wR, WR, d.r_single);
-    const uint32_t r0 = WR == 1 ? (R[0] & ru[0]) : 0u;
-    unsigned ncand = 0;
-    auto leaf = [&](int w) {
-      const uint32_t *rw = f.rowR + (int64_t)w * WR;
-      int c;
-      if (WR == 1) c = __popc(r0 & rw[0]);
-      else {
-        c = 0;
-        for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
-      }
-      ncand++;
+// Per-warp shared-memory staging of (leaf-parent slot, leaf) pairs.
+constexpr int LEAF_BUF = 256;
+struct LeafBuf {
+  uint32_t *pairs;  // [LEAF_BUF]: slot << 27 | local leaf index
+  int *wr;          // [32]: C_R word count of each slot's leaf-parent
+  int *ncand;       // [32]: leaves of each slot's leaf-parent (batch accounting)
+};
+
+// Evaluate buffered leaves: add C(|R & rowR[u] & rowR[w]|, q) (engine.py:342-347).
+template <bool INSTR>
+__device__ __forceinline__ void flush_leaves(const Params &P, const Frame &f, const Dims &d,
+                                             const uint32_t *R, const int *slot_u,
+                                             const LeafBuf &lb, int fill, Acc128 &acc,
+                                             Tally &tl) {
+  __syncwarp();
+  const int WR = d.WR, q = P.q_eff;
+  for (int p0 = 0; p0 < fill; p0 += 32) {
+    const int i = p0 + lane_id();
+    if (i < fill) {
+      const uint32_t pr = lb.pairs[i];
+      const int slot = pr >> 27, w = pr & 0x7ffffff;
+      const int u = slot_u[slot];
+      const uint32_t *ru = f.rowR + (int64_t)u * WR, *rw = f.rowR + (int64_t)w * WR;
+      int c = 0;
+      for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
       if (INSTR) {
+        const int wr = lb.wr[slot];
         tl.inter++;
         tl.opw += wr + f.adjw[w];
         tl.minw += wr < f.adjw[w] ? wr : f.adjw[w];
       }
       if (c >= q) add_comb(P, acc, c);
-    };
+    }
+  }
+  __syncwarp();
+}
+
+// Stage the leaves of one round: lane holds HTB-style word (v, pre) with
+// present bits m for leaf-parent `slot`; leaves are compacted into the pair
+// buffer (flushed 32 at a time when full).
+template <bool INSTR>
+__device__ __forceinline__ void stage_leaves(const Params &P, const Frame &f, const Dims &d,
+                                             const uint32_t *R, const int *slot_u,
+                                             const LeafBuf &lb, int &fill, int slot, uint32_t v,
+                                             int pre, uint32_t m, int wr, Acc128 &acc,
+                                             Tally &tl) {
+  const int lane = lane_id();
+  const int cnt = __popc(m);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int total = __shfl_sync(FULL, incl, 31);
+  if (fill + total > LEAF_BUF) {
+    flush_leaves<INSTR>(P, f, d, R, slot_u, lb, fill, acc, tl);
+    fill = 0;
+  }
+  if (total > LEAF_BUF) {  // a round too wide to stage: evaluate in place
+    const int WR = d.WR;
+    const uint32_t *ru = f.rowR + (int64_t)slot_u[slot] * WR;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int w = pre + __popc(v & ((1u << b) - 1u));
+      const uint32_t *rw = f.rowR + (int64_t)w * WR;
+      int c = 0;
+      for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
+      if (INSTR) {
+        tl.inter++;
+        tl.opw += wr + f.adjw[w];
+        tl.minw += wr < f.adjw[w] ? wr : f.adjw[w];
+      }
+      if (c >= P.q_eff) add_comb(P, acc, c);
+    }
+    return;
+  }
+  int o = fill + incl - cnt;
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1;
+    lb.pairs[o++] = ((uint32_t)slot << 27) | (uint32_t)(pre + __popc(v & ((1u << b) - 1u)));
+  }
+  fill += total;
+}
+
+// Leaf-parent nodes, 32 at a time (one slot per lane): node u (a survivor
+// of the node at `level`) has R' = R & rowR[u] and L' = L & rowL[u] -- or,
+// with LAZY (p_eff = 4, level 1), L' = dir2(u) & C_L1 read through the slot
+// map -- and its children are leaves (engine.py:342-347).  The L' words of
+// the 32 leaf-parents are walked as one flattened stream (LAZY: every lane
+// loads a different dir2 word each round, so the gathers overlap), and the
+// leaves are compacted and evaluated 32 at a time.
+template <bool INSTR, bool LAZY>
+__device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, const Dims &d,
+                                             int level, const int *list, int n,
+                                             const uint16_t *map, const LeafBuf &lb, Acc128 &acc,
+                                             Tally &tl) {
+  const int lane = lane_id();
+  const int WR = d.WR, WL = d.WL;
+  const uint32_t *R = f.setR + (level - 1) * WR;
+  const uint32_t *Ls = f.setL + (level - 1) * WL;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const bool act = i < n;
+    const int u = act ? list[i] : 0;
+    const int wr = act ? lane_words(R, f.rowR + (int64_t)u * WR, f.r_pre, d.wR, WR, d.r_single) : 0;
+    lb.wr[lane] = wr;
+    lb.ncand[lane] = 0;
+    __syncwarp();
+    int fill = 0;
     if (LAZY) {
-      const int id = f.lids[u];
-      const int64_t g0 = P.g.doff[id], g1 = P.g.doff[id + 1];
-      for (int64_t j = g0; j < g1; j++) {
-        const int k = map[__ldg(P.g.didx + j)];
-        if (k == 0xffff) continue;
-        const uint32_t v = f.l_val[k];
-        uint32_t m = v & __ldg(P.g.dval + j);
-        const int pre = f.l_pre[k];
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          leaf(pre + __popc(v & ((1u << b) - 1u)));
+      int64_t start = 0;
+      int len = 0;
+      if (act) {
+        const int id = f.lids[u];
+        start = P.g.doff[id];
+        len = (int)(P.g.doff[id + 1] - start);
+      }
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int excl = incl - len;
+      const int T = __shfl_sync(FULL, incl, 31);
+      for (int r0 = 0; r0 < T; r0 += 32) {
+        const int pos = r0 + lane;
+        // owning slot: the last lane whose exclusive offset is <= pos
+        int sl = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int c = sl + step;
+          const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
+          if (c < 32 && e <= pos) sl = c;
         }
+        const int64_t st = __shfl_sync(FULL, start, sl);
+        const int ex = __shfl_sync(FULL, excl, sl);
+        uint32_t m = 0, v = 0xffffffffu;
+        int pre = 0;
+        if (pos < T) {
+          const int64_t j = st + (pos - ex);
+          const uint32_t key = __ldg(P.g.didx + j), dv = __ldg(P.g.dval + j);
+          const int k = map[key];
+          if (k != 0xffff) {
+            v = f.l_val[k];
+            m = v & dv;
+            pre = f.l_pre[k];
+            if (m) atomicAdd(&lb.ncand[sl], __popc(m));
+          }
+        }
+        stage_leaves<INSTR>(P, f, d, R, list + base, lb, fill, sl, v, pre, m, lb.wr[sl], acc, tl);
       }
     } else {
+      int ncand = 0;
       const uint32_t *rl = f.rowL + (int64_t)u * WL;
-      for (int x = 0; x < WL; x++) {
-        uint32_t m = Ls[x] & rl[x];
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          leaf(x * 32 + b);
-        }
+      for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
+        uint32_t m = 0;
+        if (act && x < WL) m = Ls[x] & rl[x];
+        ncand += __popc(m);
+        stage_leaves<INSTR>(P, f, d, R, list + base, lb, fill, lane, 0xffffffffu, x * 32, m, wr,
+                            acc, tl);
       }
+      lb.ncand[lane] = ncand;
     }
-    tl.batches += node_batches(P, ncand, wr, 0, true);
+    flush_leaves<INSTR>(P, f, d, R, list + base, lb, fill, acc, tl);
+    if (act) tl.batches += node_batches(P, (unsigned)lb.ncand[lane], wr, 0, true);
+    __syncwarp();
   }
 }
 
@@ -545,7 +705,8 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
 // surv[level-1] for the depth-first descent.
 template <bool INSTR, bool LAZY>
 __device__ __forceinline__ void expand(const Params &P, const Frame &f, const Dims &d, int level,
-                                       const uint16_t *map, Acc128 &acc, Tally &tl) {
+                                       const uint16_t *map, const LeafBuf &lb, Acc128 &acc,
+                                       Tally &tl, PhaseClock &ph_) {
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL, nL = d.nL;
   const int li = level - 1;
@@ -602,7 +763,9 @@ __device__ __forceinline__ void expand(const Params &P, const Frame &f, const Di
   }
   __syncwarp();
   if (lp && ns) {
-    leaf_parents<INSTR, LAZY>(P, f, d, level, out, ns, map, acc, tl);
+    PH_MARK(4);
+    leaf_parents<INSTR, LAZY>(P, f, d, level, out, ns, map, lb, acc, tl);
+    PH_MARK(5);
     ns = 0;
   }
   if (lane == 0) {
@@ -658,11 +821,11 @@ __device__ __forceinline__ bool emit_node(const Params &P, const SplitSink &S, c
 // DFS from a node at `start` whose sets sit in setR/setL[start-1].
 template <bool INSTR, bool LAZY>
 __device__ __forceinline__ void dfs(const Params &P, const Frame &f, const Dims &d, int start,
-                                    const uint16_t *map, Acc128 &acc, Tally &tl,
-                                    const SplitSink *sink) {
+                                    const uint16_t *map, const LeafBuf &lb, Acc128 &acc, Tally &tl,
+                                    const SplitSink *sink, PhaseClock &ph_) {
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL, nL = d.nL, p_eff = P.p_eff;
-  expand<INSTR, LAZY>(P, f, d, start, map, acc, tl);
+  expand<INSTR, LAZY>(P, f, d, start, map, lb, acc, tl, ph_);
   int level = start;
   while (level >= start) {
     const int li = level - 1;
@@ -679,7 +842,7 @@ __device__ __forceinline__ void dfs(const Params &P, const Frame &f, const Dims 
       for (int w = lane; w < WL; w += 32) f.setL[(li + 1) * WL + w] = f.setL[li * WL + w] & rl[w];
       __syncwarp();
       level++;
-      expand<INSTR, LAZY>(P, f, d, level, map, acc, tl);
+      expand<INSTR, LAZY>(P, f, d, level, map, lb, acc, tl, ph_);
     } else {
       level--;
     }
@@ -690,11 +853,12 @@ __device__ __forceinline__ void dfs(const Params &P, const Frame &f, const Dims 
 // With a slot map the map is left filled for the DFS (the caller clears it).
 template <bool INSTR, bool LAZY>
 __device__ __forceinline__ void build_frame(const Params &P, const Frame &f, const Dims &d, int r,
-                                            int s, uint16_t *map) {
+                                            int s, uint16_t *map, PhaseClock &ph_) {
   const int lane = lane_id();
   int card;
   isect_adj<true>(P.g, r, s, card, f.r_idx, f.r_val, f.r_pre);
   isect_dir<true>(P.g, r, s, card, f.l_idx, f.l_val, f.l_pre);
+  PH_MARK(1);
   // decode C_L1 ids (ascending, htb.py:42-52); fill the slot map
   for (int k = lane; k < d.wL; k += 32) {
     uint32_t v = f.l_val[k];
@@ -707,6 +871,7 @@ __device__ __forceinline__ void build_frame(const Params &P, const Frame &f, con
     }
   }
   __syncwarp();
+  PH_MARK(2);
   for (int x = lane; x < d.nL; x += 32) {
     const int id = f.lids[x];
     const int64_t a0 = P.g.aoff[id], a1 = P.g.aoff[id + 1];
@@ -729,6 +894,7 @@ __device__ __forceinline__ void build_frame(const Params &P, const Frame &f, con
     }
   }
   __syncwarp();
+  PH_MARK(3);
 }
 
 __device__ __forceinline__ void clear_map(uint16_t *map, const Frame &f, const Dims &d) {
@@ -902,20 +1068,25 @@ __device__ __forceinline__ void flush_tallies(const Params &P, const Acc128 &tot
 }
 
 constexpr int ENUM_THREADS = 256;
+#ifndef ENUM_MIN_BLOCKS
+#define ENUM_MIN_BLOCKS 3
+#endif
+constexpr int LEAF_WORDS = LEAF_BUF + 64;  // per-warp leaf staging in shared memory
 
 // Whole tasks (SPLIT = false) or the top levels of every task with its frame
 // written to the global frame arena and split-level nodes pushed as sub-tasks
 // (SPLIT = true, p_eff >= 5).
 template <bool INSTR, bool LAZY, bool SPLIT>
-__global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArgs A) {
+__global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Params P, EnumArgs A) {
   extern __shared__ uint32_t smem[];
   const int lane = lane_id();
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int map_w = (P.map_words + 1) / 2;  // u16 entries packed in words
-  uint32_t *my = smem + (int64_t)wib * (map_w + A.budget_words);
+  uint32_t *my = smem + (int64_t)wib * (map_w + LEAF_WORDS + A.budget_words);
   uint16_t *map = P.map_words ? (uint16_t *)my : nullptr;
-  uint32_t *my_smem = my + map_w;
+  const LeafBuf lb{my + map_w, (int *)(my + map_w + LEAF_BUF), (int *)(my + map_w + LEAF_BUF + 32)};
+  uint32_t *my_smem = my + map_w + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   if (map)
     for (int i = lane; i < map_w; i += 32) my[i] = 0xffffffffu;
@@ -924,10 +1095,12 @@ __global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArg
   Tally tl;
   unsigned long long claims = 0, spills = 0;
   const int p_eff = P.p_eff;
+  PH_DECL
   for (;;) {
     long long qi = 0;
     if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
     qi = __shfl_sync(FULL, qi, 0) + A.q0;
+    PH_MARK(0);
     if (qi >= A.q1) break;
     claims++;
     const int j = A.queue[qi];
@@ -957,36 +1130,42 @@ __global__ void __launch_bounds__(ENUM_THREADS, 2) enum_kernel(Params P, EnumArg
     Frame f;
     carve_ro(f, ro_base, d, rowL, INSTR);
     carve_scratch(f, sc_base, d, p_eff);
-    build_frame<INSTR, LAZY>(P, f, d, tk.x, tk.y, map);
+    build_frame<INSTR, LAZY>(P, f, d, tk.x, tk.y, map, ph_);
     init_root_sets(f, d);
     Acc128 acc{0, 0};
     if (SPLIT) {
       SplitSink sink = A.sink;
       sink.frame_off = A.frame_off[qi - A.q0];
       sink.task_j = j;
-      dfs<INSTR, false>(P, f, d, 1, map, acc, tl, &sink);
+      dfs<INSTR, false>(P, f, d, 1, map, lb, acc, tl, &sink, ph_);
     } else {
-      dfs<INSTR, LAZY>(P, f, d, 1, map, acc, tl, nullptr);
+      dfs<INSTR, LAZY>(P, f, d, 1, map, lb, acc, tl, nullptr, ph_);
     }
+    PH_MARK(4);
     clear_map(map, f, d);
     finish_task(P, acc, t, SPLIT, total);
+    PH_MARK(6);
   }
+  PH_FLUSH();
   flush_tallies(P, total, tl, claims, spills, INSTR);
 }
 
 // Split nodes: warp per sub-task record, records in LPT order.
 template <bool INSTR>
-__global__ void __launch_bounds__(ENUM_THREADS, 2) sub_kernel(Params P, EnumArgs A, int64_t n_sub) {
+__global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Params P, EnumArgs A, int64_t n_sub) {
   extern __shared__ uint32_t smem[];
   const int lane = lane_id();
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  uint32_t *my_smem = smem + (int64_t)wib * A.budget_words;
+  uint32_t *my = smem + (int64_t)wib * (LEAF_WORDS + A.budget_words);
+  const LeafBuf lb{my, (int *)(my + LEAF_BUF), (int *)(my + LEAF_BUF + 32)};
+  uint32_t *my_smem = my + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   Acc128 total{0, 0};
   Tally tl;
   unsigned long long spills = 0;
   const int p_eff = P.p_eff;
+  PH_DECL
   for (;;) {
     long long k = 0;
     if (lane == 0) k = (long long)atomicAdd(P.ctr + CTR_SUB_NEXT, 1ull);
@@ -1012,9 +1191,13 @@ __global__ void __launch_bounds__(ENUM_THREADS, 2) sub_kernel(Params P, EnumArgs
     for (int w = lane; w < d.WL; w += 32) f.setL[(lv - 1) * d.WL + w] = rec[4 + d.WR + w];
     __syncwarp();
     Acc128 acc{0, 0};
-    dfs<INSTR, false>(P, f, d, lv, nullptr, acc, tl, nullptr);
+    PH_MARK(0);
+    dfs<INSTR, false>(P, f, d, lv, nullptr, lb, acc, tl, nullptr, ph_);
+    PH_MARK(4);
     finish_task(P, acc, t, true, total);
+    PH_MARK(6);
   }
+  PH_FLUSH();
   flush_tallies(P, total, tl, 0, spills, INSTR);
 }
 
@@ -1088,6 +1271,11 @@ T sum_device(const T *p, int64_t n, cudaStream_t st) {
   copy_d2h(&h, out.p, sizeof(T), st);
   BC_CUDA(cudaStreamSynchronize(st));
   return h;
+}
+
+int env_int(const char *name, int dflt) {  // development knobs
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 template <typename K, typename V>
@@ -1225,8 +1413,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
         if (!split) {
           // whole tasks per warp; frames in shared memory
           const bool lazy = s.p_eff == 4 && !has_rowL(s.p_eff, P.map_words);
-          const int budget = 2048;
-          const size_t smem = (size_t)wpb * (budget + map_w) * 4;
+          const int budget = env_int("BC_ENUM_BUDGET", 1200);
+          const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
           auto kern = instr ? (lazy ? enum_kernel<true, true, false> : enum_kernel<true, false, false>)
                             : (lazy ? enum_kernel<false, true, false> : enum_kernel<false, false, false>);
           const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
@@ -1247,11 +1435,11 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           // writes every frame to the frame arena and pushes the split-level nodes,
           // then sub_kernel drains them heaviest first with every warp.
           const int split_level = s.p_eff <= 6 ? 2 : 3;
-          const int budget = 1024;
-          const size_t smem = (size_t)wpb * (budget + map_w) * 4;
+          const int budget = env_int("BC_SPLIT_BUDGET", 1024);
+          const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
           auto kern = instr ? enum_kernel<true, false, true> : enum_kernel<false, false, true>;
           auto sk = instr ? sub_kernel<true> : sub_kernel<false>;
-          const size_t ssmem = (size_t)wpb * budget * 4;
+          const size_t ssmem = (size_t)wpb * (budget + LEAF_WORDS) * 4;
           const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
           const int64_t sblocks = std::min<int64_t>((int64_t)sms * blocks_per_sm(sk, ssmem), blocks);
           A.budget_words = budget;
