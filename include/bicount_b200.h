@@ -67,6 +67,11 @@ typedef struct bc_config {
 #define BC_FLAG_INSTRUMENT 2    /* tally reference-equivalent intersections / operand
                                    words (B_enum, B_min) on device */
 #define BC_FLAG_NO_SPLIT 4      /* disable heavy-task splitting (tests) */
+#define BC_FLAG_L1_SCATTER 8    /* level 1 by root-grouped wedge scatter (default: chosen
+                                   by a cost estimate) */
+#define BC_FLAG_L1_PROBE 16     /* level 1 by per-task HTB intersections */
+#define BC_FLAG_ROWR_SCATTER 32 /* candidate rows by wedge scatter where a slot map exists */
+#define BC_FLAG_ROWR_PROBE 64   /* candidate rows by per-candidate intersections */
 
 /* CountReport (engine.py:64-79) plus device measurements. */
 typedef struct bc_report {
@@ -128,6 +133,12 @@ int bc_count(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
 int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
                     const int64_t *v_off, const int32_t *v_idx, int64_t n_v,
                     int32_t device, bc_graph **out);
+/* Same, from CSR arrays already resident on `device` (e.g. a graph generated on the
+ * GPU): device-to-device copy, no host round trip.  Not in the reference (its graphs
+ * are host lists); used for the FR-scale config, whose 1e8-edge CSR is built on device. */
+int bc_graph_create_device(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
+                           const int64_t *v_off, const int32_t *v_idx, int64_t n_v,
+                           int32_t device, bc_graph **out);
 int bc_graph_count(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg, bc_report *out);
 void bc_graph_destroy(bc_graph *g);
 

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("BC_LIB") or os.path.join(HERE, "libbicount_b200.so")
 
 BC_OK, BC_EINVAL, BC_ECUDA, BC_ENCCL, BC_EOOM, BC_EOVERFLOW = 0, -1, -2, -3, -4, -5
 BC_FLAG_TASK_COUNTS, BC_FLAG_INSTRUMENT, BC_FLAG_NO_SPLIT = 1, 2, 4
+BC_FLAG_L1_SCATTER, BC_FLAG_L1_PROBE, BC_FLAG_ROWR_SCATTER, BC_FLAG_ROWR_PROBE = 8, 16, 32, 64
 
 (BC_X_UND_SIZE, BC_X_RANK, BC_X_ORDER, BC_X_DIR_OFF, BC_X_DIR_IDX, BC_X_HADJ_OFF,
  BC_X_HADJ_IDX, BC_X_HADJ_VAL, BC_X_HDIR_OFF, BC_X_HDIR_IDX, BC_X_HDIR_VAL, BC_X_TASKS,
@@ -22,7 +23,7 @@ BC_FLAG_TASK_COUNTS, BC_FLAG_INSTRUMENT, BC_FLAG_NO_SPLIT = 1, 2, 4
 
 # every symbol include/bicount_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("bc_abi_version", "bc_last_error", "bc_device_count", "bc_count", "bc_graph_create",
-            "bc_graph_count", "bc_graph_destroy", "bc_prepare", "bc_export_len", "bc_export",
+            "bc_graph_create_device", "bc_graph_count", "bc_graph_destroy", "bc_prepare", "bc_export_len", "bc_export",
             "bc_structs_destroy", "bc_shutdown", "bc_debug_phase_cycles")
 
 
@@ -72,6 +73,8 @@ def _declare(L):
                            C.POINTER(BcReport)]
     L.bc_graph_create.restype = C.c_int
     L.bc_graph_create.argtypes = [vp, vp, i64, vp, vp, i64, i32, C.POINTER(C.c_void_p)]
+    L.bc_graph_create_device.restype = C.c_int
+    L.bc_graph_create_device.argtypes = [vp, vp, i64, vp, vp, i64, i32, C.POINTER(C.c_void_p)]
     L.bc_graph_count.restype = C.c_int
     L.bc_graph_count.argtypes = [vp, i32, i32, C.POINTER(BcConfig), C.POINTER(BcReport)]
     L.bc_graph_destroy.restype = None

@@ -47,19 +47,37 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     lib = out or LIB
     if not force and out is None and up_to_date():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-           "--expt-relaxed-constexpr", "-shared", "-o", lib + ".tmp", *sources(),
-           "-lcudart"]
+    # one nvcc per translation unit in parallel, then one link
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+             "--expt-relaxed-constexpr", *(extra or [])]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    if extra:
-        cmd[1:1] = extra
-    r = subprocess.run(cmd, capture_output=True, text=True)
+        flags.insert(0, "-Xptxas=-v")
+    tag = os.path.basename(lib).replace(".so", "")
+    objs, procs = [], []
+    for src in sources():
+        obj = os.path.join(CSRC, f".{tag}.{os.path.basename(src)}.o")
+        objs.append(obj)
+        procs.append((src, subprocess.Popen([nvcc(), *flags, "-c", "-o", obj, src],
+                                            stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+    failed = False
+    for src, pr in procs:
+        out_, err_ = pr.communicate()
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(out_ + err_)
+        elif verbose:
+            sys.stderr.write(err_)
+    if failed:
+        raise RuntimeError("nvcc build of libbicount_b200.so failed")
+    r = subprocess.run([nvcc(), *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"],
+                       capture_output=True, text=True)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libbicount_b200.so failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("link of libbicount_b200.so failed")
     os.replace(lib + ".tmp", lib)
     return lib
 

@@ -98,17 +98,28 @@ int bc_device_count(void) {
   return n;
 }
 
-int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
-                    const int64_t *v_off, const int32_t *v_idx, int64_t n_v, int32_t device,
-                    bc_graph **out) {
+static int graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
+                        const int64_t *v_off, const int32_t *v_idx, int64_t n_v, int32_t device,
+                        bool on_device, bc_graph **out) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_err.clear();
   *out = nullptr;
   if (n_u < 0 || n_v < 0 || !u_off || !v_off) return fail(BC_EINVAL, "invalid graph arrays");
   if (n_u >= (int64_t(1) << 31) || n_v >= (int64_t(1) << 31))
     return fail(BC_EINVAL, "layer sizes must be < 2^31");
-  const int64_t e = u_off[n_u];
-  if (v_off[n_v] != e) return fail(BC_EINVAL, "U and V views disagree on the edge count");
+  int64_t e = 0, ev = 0;
+  if (on_device) {
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaMemcpy(&e, u_off + n_u, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&ev, v_off + n_v, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(BC_ECUDA, "cannot read device CSR offsets");
+    }
+  } else {
+    e = u_off[n_u];
+    ev = v_off[n_v];
+  }
+  if (ev != e) return fail(BC_EINVAL, "U and V views disagree on the edge count");
   bc_graph *h = new bc_graph();
   try {
     bc::DevGraph &g = h->g;
@@ -132,11 +143,20 @@ int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
     BC_CUDA(cudaMallocAsync((void **)&g.v_off, (n_v + 1) * 8, st));
     BC_CUDA(cudaMallocAsync((void **)&g.u_idx, (e ? e : 1) * 4, st));
     BC_CUDA(cudaMallocAsync((void **)&g.v_idx, (e ? e : 1) * 4, st));
-    bc::copy_h2d(g.u_off, u_off, (n_u + 1) * 8, st);
-    bc::copy_h2d(g.v_off, v_off, (n_v + 1) * 8, st);
-    if (e) {
-      bc::copy_h2d(g.u_idx, u_idx, e * 4, st);
-      bc::copy_h2d(g.v_idx, v_idx, e * 4, st);
+    if (on_device) {  // device-resident input (e.g. a torch CUDA tensor): D2D copy
+      BC_CUDA(cudaMemcpyAsync(g.u_off, u_off, (n_u + 1) * 8, cudaMemcpyDeviceToDevice, st));
+      BC_CUDA(cudaMemcpyAsync(g.v_off, v_off, (n_v + 1) * 8, cudaMemcpyDeviceToDevice, st));
+      if (e) {
+        BC_CUDA(cudaMemcpyAsync(g.u_idx, u_idx, e * 4, cudaMemcpyDeviceToDevice, st));
+        BC_CUDA(cudaMemcpyAsync(g.v_idx, v_idx, e * 4, cudaMemcpyDeviceToDevice, st));
+      }
+    } else {
+      bc::copy_h2d(g.u_off, u_off, (n_u + 1) * 8, st);
+      bc::copy_h2d(g.v_off, v_off, (n_v + 1) * 8, st);
+      if (e) {
+        bc::copy_h2d(g.u_idx, u_idx, e * 4, st);
+        bc::copy_h2d(g.v_idx, v_idx, e * 4, st);
+      }
     }
     // wedge mass + max degree per layer (graph.py:246-249), once per graph
     unsigned long long *dw;
@@ -166,6 +186,18 @@ int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
   }
   *out = h;
   return BC_OK;
+}
+
+int bc_graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
+                    const int64_t *v_off, const int32_t *v_idx, int64_t n_v, int32_t device,
+                    bc_graph **out) {
+  return graph_create(u_off, u_idx, n_u, v_off, v_idx, n_v, device, false, out);
+}
+
+int bc_graph_create_device(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
+                           const int64_t *v_off, const int32_t *v_idx, int64_t n_v,
+                           int32_t device, bc_graph **out) {
+  return graph_create(u_off, u_idx, n_u, v_off, v_idx, n_v, device, true, out);
 }
 
 void bc_graph_destroy(bc_graph *h) {

@@ -86,6 +86,9 @@ struct DevStructs {
   DBuf<int64_t> hadj_off, hdir_off;
   DBuf<uint32_t> hadj_idx, hadj_val, hdir_idx, hdir_val;
   DBuf<int2> tasks;  // (root, second) in emission order
+  // first task id of each anchor vertex's tasks (-1 if it roots none): the tasks of
+  // root r are troot[r] + j for its j-th dir2 entry (engine.py:160-172)
+  DBuf<int64_t> troot;
   // dense bitmaps of the longest adjacency rows (hubs): dense[slot * dense_mw + w] is the
   // HTB Val of word w (0 if absent); dense_id[x] = slot or -1
   DBuf<int32_t> dense_id;

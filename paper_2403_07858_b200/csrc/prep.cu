@@ -380,6 +380,12 @@ __global__ void task_write(const int64_t *__restrict__ order, const int64_t *__r
   }
 }
 
+__global__ void root_task_off(const int64_t *__restrict__ order, const int64_t *__restrict__ toff,
+                              const int64_t *__restrict__ cnt, int64_t n, int64_t *__restrict__ troot) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) troot[order[i]] = cnt[i] ? toff[i] : -1;
+}
+
 __global__ void max_reduce(const int64_t *a, int64_t n, unsigned long long *out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned long long v = i < n ? (unsigned long long)a[i] : 0;
@@ -699,7 +705,10 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     if (n > 0 && s.emitted)
       task_write<<<warp_blocks(n, sms), 256, 0, st>>>(s.order.p, toff.p, cnt.p, s.dir_off.p,
                                                       s.dir_idx.p, n, s.p_eff, s.tasks.p);
-    L += 3;
+    s.troot.alloc(n ? n : 1, st);
+    if (n > 0)
+      root_task_off<<<blocks_for(n, 256), 256, 0, st>>>(s.order.p, toff.p, cnt.p, n, s.troot.p);
+    L += 4;
   }
   tm.mark("tasks");
   (void)p;

@@ -38,6 +38,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <ctime>
 #include <cstdlib>
 #include <vector>
 
@@ -109,6 +110,8 @@ struct Graph2 {  // HTB arenas (htb.py:64-86) + dense hub rows
   const int32_t *__restrict__ dense_id;
   const uint32_t *__restrict__ dense;
   int64_t mw;
+  const int64_t *__restrict__ boff;  // opposite layer -> anchor CSR (graph.py:15-49 v_adj
+  const int32_t *__restrict__ bidx;  // of the work graph): the wedge-scatter rows
 };
 
 struct Params {
@@ -126,11 +129,14 @@ struct Params {
   unsigned long long *ctr;              // counters, see CTR_*
   unsigned long long *task_counts;      // optional [2 * n_tasks]
   int map_words;                        // anchor-word slot map entries (0 = no map)
+  const int64_t *__restrict__ roff;     // wedge-scatter level 1: C_R1 of local task j is
+  const int32_t *__restrict__ lists;    //   lists[roff[j], roff[j+1]) (ascending ids), or null
+  int rowR_mode;                        // 0 = per-task choice, 1 = scatter, 2 = probe
 };
 
 enum { CTR_ALIVE = 0, CTR_BATCHES, CTR_STOLEN, CTR_INTER, CTR_OPW, CTR_MINW, CTR_MAXRO,
        CTR_MAXSCR, CTR_SPILL, CTR_NEXT, CTR_SUB_USED, CTR_SUB_N, CTR_SUB_NEXT, CTR_SPLIT,
-       CTR_COUNT };
+       CTR_HEAVY, CTR_MAXRO_T, CTR_MAXSCR_T, CTR_COUNT };
 
 struct Info {  // level-1 facts of one task
   int32_t cr, wr, cl, wl;
@@ -255,19 +261,23 @@ __device__ __forceinline__ int isect_dir(const Graph2 &g, int r, int s, int &car
 
 // Frame: the task-local universe.  The read-only part (built once) and the
 // per-warp DFS scratch are carved separately so split tasks can share the
-// former from global memory.
+// former from global memory.  rowL rows exist only for the level-1
+// R-survivors (x with |rowR[x]| >= q): every candidate whose rowL is ever read
+// has passed |R & rowR[x]| >= q at some node, and R is a subset of C_R1, so it
+// passed at level 1 too; lslot[x] is its rowL row (-1: none).
 struct Frame {
   uint32_t *r_idx, *r_val;
   int *r_pre;
   uint32_t *l_idx, *l_val;
   int *l_pre;
-  int *lids;
+  int *lids, *lslot;
   uint32_t *rowR, *rowL;
   int *adjw, *dirw;
   int *cand;
   uint32_t *setR, *setL;
   int *surv;
   int *ns, *cur;
+  int surv_cap;
 };
 
 // rowL is materialised for p_eff >= 5 (reused at every depth) and for p_eff = 4
@@ -276,13 +286,18 @@ __host__ __device__ __forceinline__ bool has_rowL(int p_eff, int map_words) {
   return p_eff >= 5 || (p_eff == 4 && map_words == 0);
 }
 
+// rowL rows allocated: level-1 R-survivors, bounded by nL (or by the triage cap).
+__host__ __device__ __forceinline__ int64_t rowl_rows(int nL, bool rowL, int cap) {
+  return rowL ? (cap > 0 && cap < nL ? cap : nL) : 0;
+}
+
 __host__ __device__ __forceinline__ int64_t ro_words(int nR, int nL, int wR, int wL, bool rowL,
-                                                     bool instr) {
+                                                     bool instr, int cap = 0) {
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
   int64_t w = 3 * (int64_t)wR + 1 + 3 * (int64_t)wL + 1;  // C_R1 / C_L1 HTB words + prefixes
-  w += nL;                                                 // lids
+  w += 2 * (int64_t)nL;                                    // lids, lslot
   w += (int64_t)nL * WR;                                   // rowR
-  if (rowL) w += (int64_t)nL * WL;                         // rowL
+  w += rowl_rows(nL, rowL, cap) * WL;                      // rowL
   if (instr) w += 2 * (int64_t)nL;                         // adj / dir2 slice words
   return (w + 3) & ~int64_t(3);
 }
@@ -293,14 +308,19 @@ __host__ __device__ __forceinline__ int stack_levels(int p_eff) {
   return p_eff - 3 > 1 ? p_eff - 3 : 1;
 }
 
-__host__ __device__ __forceinline__ int64_t scratch_words(int nR, int nL, int p_eff) {
+// survivors listed per level: level-1 R-survivors, bounded by nL (or the triage cap)
+__host__ __device__ __forceinline__ int surv_cap_of(int nL, int cap) {
+  return cap > 0 && cap < nL ? cap : nL;
+}
+
+__host__ __device__ __forceinline__ int64_t scratch_words(int nR, int nL, int p_eff, int cap = 0) {
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
   const int64_t levels = stack_levels(p_eff);
-  return ((int64_t)nL + levels * (WR + WL + nL + 2) + 3) & ~int64_t(3);
+  return ((int64_t)nL + levels * (WR + WL + surv_cap_of(nL, cap) + 2) + 3) & ~int64_t(3);
 }
 
 __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d, bool rowL,
-                                         bool instr) {
+                                         bool instr, int cap = 0) {
   f.r_idx = p; p += d.wR;
   f.r_val = p; p += d.wR;
   f.r_pre = (int *)p; p += d.wR + 1;
@@ -308,20 +328,27 @@ __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d, b
   f.l_val = p; p += d.wL;
   f.l_pre = (int *)p; p += d.wL + 1;
   f.lids = (int *)p; p += d.nL;
+  f.lslot = (int *)p; p += d.nL;
   f.rowR = p; p += (int64_t)d.nL * d.WR;
-  f.rowL = p; if (rowL) p += (int64_t)d.nL * d.WL;
+  f.rowL = p; p += rowl_rows(d.nL, rowL, cap) * d.WL;
   f.adjw = (int *)p; if (instr) p += d.nL;
   f.dirw = (int *)p;
 }
 
-__device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims &d, int p_eff) {
+__device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims &d, int p_eff,
+                                              int cap = 0) {
   const int levels = stack_levels(p_eff);
+  f.surv_cap = surv_cap_of(d.nL, cap);
   f.cand = (int *)p; p += d.nL;
   f.setR = p; p += (int64_t)levels * d.WR;
   f.setL = p; p += (int64_t)levels * d.WL;
-  f.surv = (int *)p; p += (int64_t)levels * d.nL;
+  f.surv = (int *)p; p += (int64_t)levels * f.surv_cap;
   f.ns = (int *)p; p += levels;
   f.cur = (int *)p;
+}
+
+__device__ __forceinline__ const uint32_t *rowL_of(const Frame &f, const Dims &d, int u) {
+  return f.rowL + (int64_t)f.lslot[u] * d.WL;
 }
 
 // Writes a local-universe row whose set positions arrive in ascending order:
@@ -683,7 +710,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
       }
     } else {
       int ncand = 0;
-      const uint32_t *rl = f.rowL + (int64_t)u * WL;
+      const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL;
       for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
         uint32_t m = 0;
         if (act && x < WL) m = Ls[x] & rl[x];
@@ -720,7 +747,7 @@ __device__ __forceinline__ void expand(const Params &P, const Frame &f, const Di
   if (lane == 0) tl.batches += node_batches(P, (unsigned)ncand, wr, wl, leaf);
   int ns = 0;
   const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
-  int *out = f.surv + li * nL;
+  int *out = f.surv + li * f.surv_cap;
   for (int c0 = 0; c0 < ncand; c0 += 32) {
     const int i = c0 + lane;
     bool keep = false;
@@ -747,7 +774,7 @@ __device__ __forceinline__ void expand(const Params &P, const Frame &f, const Di
           if (LAZY) {
             keep = true;  // |L'| >= 1 is checked when the leaf-parent is walked
           } else {
-            const uint32_t *rl = f.rowL + (int64_t)u * WL;
+            const uint32_t *rl = rowL_of(f, d, u);
             int cl = 0;
             for (int w = 0; w < WL; w++) cl += __popc(Ls[w] & rl[w]);
             keep = cl >= need_l;
@@ -830,11 +857,11 @@ __device__ __forceinline__ void dfs(const Params &P, const Frame &f, const Dims 
   while (level >= start) {
     const int li = level - 1;
     if (level + 1 < p_eff - 2 && f.cur[li] < f.ns[li]) {
-      const int u = f.surv[li * nL + f.cur[li]];
+      const int u = f.surv[li * f.surv_cap + f.cur[li]];
       __syncwarp();
       if (lane == 0) f.cur[li]++;
       const uint32_t *rr = f.rowR + (int64_t)u * WR;
-      const uint32_t *rl = f.rowL + (int64_t)u * WL;
+      const uint32_t *rl = rowL_of(f, d, u);
       if (sink && level + 1 == sink->level &&
           emit_node(P, *sink, d, level + 1, f.setR + li * WR, rr, f.setL + li * WL, rl))
         continue;
@@ -849,14 +876,88 @@ __device__ __forceinline__ void dfs(const Params &P, const Frame &f, const Dims 
   }
 }
 
-// Build the read-only frame of task (r, s) at f (engine.py:277-292, 338, 360).
-// With a slot map the map is left filled for the DFS (the caller clears it).
-template <bool INSTR, bool LAZY>
-__device__ __forceinline__ void build_frame(const Params &P, const Frame &f, const Dims &d, int r,
-                                            int s, uint16_t *map, PhaseClock &ph_) {
+// Sorted id list -> HTB words (htb.py:89-115) with exclusive prefix
+// popcounts (o_pre[words] = n); returns the word count.
+__device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int n,
+                                           uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
+  const int lane = lane_id();
+  int pos = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    uint32_t word = 0;
+    bool start = false;
+    if (i < n) {
+      word = (uint32_t)__ldg(ids + i) >> 5;
+      start = i == 0 || ((uint32_t)__ldg(ids + i - 1) >> 5) != word;
+    }
+    const unsigned m = __ballot_sync(FULL, start);
+    if (start) {
+      uint32_t v = 0;
+      for (int k = i; k < n; k++) {
+        const uint32_t id = (uint32_t)__ldg(ids + k);
+        if ((id >> 5) != word) break;
+        v |= 1u << (id & 31);
+      }
+      const int o = pos + __popc(m & lanemask_lt());
+      o_idx[o] = word;
+      o_val[o] = v;
+      o_pre[o] = i;
+    }
+    pos += __popc(m);
+  }
+  if (lane == 0) o_pre[pos] = n;
+  __syncwarp();
+  return pos;
+}
+
+// rowR by wedge scatter: for every C_R1 member v (local index i, ascending id
+// order) and every anchor x in N(v) that lies in C_L1 (slot map), set bit i of
+// rowR[x].  Work is sum_{v in C_R1} deg(v) over contiguous opposite-layer rows
+// instead of |C_L1| probes of (possibly hub-sized) adjacency rows.
+__device__ __forceinline__ void scatter_rowR(const Params &P, const Frame &f, const Dims &d,
+                                             const uint16_t *map) {
+  const int lane = lane_id();
+  const int64_t total = (int64_t)d.nL * d.WR;
+  for (int64_t w = lane; w < total; w += 32) f.rowR[w] = 0;
+  __syncwarp();
+  for (int k = lane; k < d.wR; k += 32) {
+    uint32_t bits = f.r_val[k];
+    const int64_t vb = (int64_t)f.r_idx[k] * 32;
+    int i = f.r_pre[k];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int64_t v = vb + b;
+      const uint32_t ibit = 1u << (i & 31);
+      const int iw = i >> 5;
+      for (int64_t e = __ldg(P.g.boff + v), e1 = __ldg(P.g.boff + v + 1); e < e1; e++) {
+        const int x = __ldg(P.g.bidx + e);
+        const int kk = map[x >> 5];
+        if (kk == 0xffff) continue;
+        const uint32_t lv = f.l_val[kk];
+        const int xb = x & 31;
+        if (!((lv >> xb) & 1u)) continue;
+        const int lx = f.l_pre[kk] + __popc(lv & ((1u << xb) - 1u));
+        atomicOr(f.rowR + (int64_t)lx * d.WR + iw, ibit);
+      }
+      i++;
+    }
+  }
+  __syncwarp();
+}
+
+// Frame part 1 for task (r, s) (local index j): C_R1 / C_L1 (engine.py:277-292)
+// -- C_R1 from the wedge-scatter level-1 lists when present -- the decoded C_L1
+// ids + slot map, and rowR[x] = N(x) & C_R1 for x in C_L1 (engine.py:338).
+// Returns the number of level-1 R-survivors (|rowR[x]| >= q).
+template <bool INSTR>
+__device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, const Dims &d,
+                                             int r, int s, int64_t j, uint16_t *map,
+                                             PhaseClock &ph_) {
   const int lane = lane_id();
   int card;
-  isect_adj<true>(P.g, r, s, card, f.r_idx, f.r_val, f.r_pre);
+  if (P.lists) list_to_htb(P.lists + P.roff[j], d.nR, f.r_idx, f.r_val, f.r_pre);
+  else isect_adj<true>(P.g, r, s, card, f.r_idx, f.r_val, f.r_pre);
   isect_dir<true>(P.g, r, s, card, f.l_idx, f.l_val, f.l_pre);
   PH_MARK(1);
   // decode C_L1 ids (ascending, htb.py:42-52); fill the slot map
@@ -872,26 +973,85 @@ __device__ __forceinline__ void build_frame(const Params &P, const Frame &f, con
   }
   __syncwarp();
   PH_MARK(2);
+  bool scatter = false;
+  if (map && P.rowR_mode != 2) {
+    if (P.rowR_mode == 1) {
+      scatter = true;
+    } else {
+      // sum of C_R1 members' degrees vs ~2 probes per (x, C_R1 word)
+      long long sdeg = 0;
+      for (int k = lane; k < d.wR; k += 32) {
+        uint32_t bits = f.r_val[k];
+        const int64_t vb = (int64_t)f.r_idx[k] * 32;
+        while (bits) {
+          const int64_t v = vb + __ffs(bits) - 1;
+          bits &= bits - 1;
+          sdeg += __ldg(P.g.boff + v + 1) - __ldg(P.g.boff + v);
+        }
+      }
+      sdeg = warp_sum(sdeg);
+      scatter = sdeg < 2ll * d.nL * d.wR;
+    }
+  }
+  if (scatter) {
+    scatter_rowR(P, f, d, map);
+  } else {
+    for (int x = lane; x < d.nL; x += 32) {
+      const int id = f.lids[x];
+      const int sl = P.g.dense_id[id];
+      local_row(f.r_idx, f.r_val, f.r_pre, d.wR, P.g.aidx, P.g.aval, P.g.aoff[id],
+                P.g.aoff[id + 1], sl >= 0 ? P.g.dense + (int64_t)sl * P.g.mw : nullptr,
+                f.rowR + (int64_t)x * d.WR, d.WR);
+    }
+    __syncwarp();
+  }
+  int ns1 = 0;
   for (int x = lane; x < d.nL; x += 32) {
-    const int id = f.lids[x];
-    const int64_t a0 = P.g.aoff[id], a1 = P.g.aoff[id + 1];
-    const int sl = P.g.dense_id[id];
-    local_row(f.r_idx, f.r_val, f.r_pre, d.wR, P.g.aidx, P.g.aval, a0, a1,
-              sl >= 0 ? P.g.dense + (int64_t)sl * P.g.mw : nullptr, f.rowR + (int64_t)x * d.WR,
-              d.WR);
-    const int64_t d0 = P.g.doff[id], d1 = P.g.doff[id + 1];
-    if (P.p_eff >= 4 && !LAZY) {
-      if (map)
-        local_row_map(map, f.l_val, f.l_pre, P.g.didx, P.g.dval, d0, d1,
-                      f.rowL + (int64_t)x * d.WL, d.WL);
-      else
-        local_row(f.l_idx, f.l_val, f.l_pre, d.wL, P.g.didx, P.g.dval, d0, d1, nullptr,
-                  f.rowL + (int64_t)x * d.WL, d.WL);
+    const uint32_t *row = f.rowR + (int64_t)x * d.WR;
+    int c = 0;
+    for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
+    ns1 += c >= P.q_eff;
+  }
+  return __reduce_add_sync(FULL, ns1);
+}
+
+// Frame part 2: rowL[x] = dir2(x) & C_L1 (engine.py:360) for the level-1
+// R-survivors only (lslot), and the slice lengths the instrumented tallies use.
+template <bool INSTR, bool LAZY>
+__device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, const Dims &d,
+                                              const uint16_t *map, bool rowL, PhaseClock &ph_) {
+  const int lane = lane_id();
+  const bool build = rowL && P.p_eff >= 4 && !LAZY;
+  int base = 0;
+  for (int x0 = 0; x0 < d.nL; x0 += 32) {
+    const int x = x0 + lane;
+    bool sv = false;
+    if (x < d.nL) {
+      const uint32_t *row = f.rowR + (int64_t)x * d.WR;
+      int c = 0;
+      for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
+      sv = c >= P.q_eff;
     }
-    if (INSTR) {
-      f.adjw[x] = (int)(a1 - a0);
-      f.dirw[x] = (int)(d1 - d0);
+    const unsigned m = __ballot_sync(FULL, sv);
+    if (x < d.nL) {
+      const int slot = sv ? base + __popc(m & lanemask_lt()) : -1;
+      f.lslot[x] = slot;
+      const int id = f.lids[x];
+      if (build && sv) {
+        const int64_t d0 = P.g.doff[id], d1 = P.g.doff[id + 1];
+        uint32_t *out = f.rowL + (int64_t)slot * d.WL;
+        if (map)
+          local_row_map(map, f.l_val, f.l_pre, P.g.didx, P.g.dval, d0, d1, out, d.WL);
+        else
+          local_row(f.l_idx, f.l_val, f.l_pre, d.wL, P.g.didx, P.g.dval, d0, d1, nullptr, out,
+                    d.WL);
+      }
+      if (INSTR) {
+        f.adjw[x] = (int)(P.g.aoff[id + 1] - P.g.aoff[id]);
+        f.dirw[x] = (int)(P.g.doff[id + 1] - P.g.doff[id]);
+      }
     }
+    base += __popc(m);
   }
   __syncwarp();
   PH_MARK(3);
@@ -954,8 +1114,23 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
   for (int64_t j = gw; j < nloc; j += nw) {
     const int64_t t = P.shard + j * P.nshards;
     const int2 tk = P.tasks[t];
-    int cr;
-    const int wr = isect_adj<false>(P.g, tk.x, tk.y, cr, nullptr, nullptr, nullptr);
+    int cr, wr;
+    if (P.lists) {  // C_R1 from the wedge-scatter pass: |C_R1| and its HTB word count
+      const int64_t l0 = P.roff[j];
+      cr = (int)(P.roff[j + 1] - l0);
+      wr = 0;
+      for (int b = 0; b < cr; b += 32) {
+        const int i = b + lane;
+        bool start = false;
+        if (i < cr) {
+          const uint32_t w = (uint32_t)__ldg(P.lists + l0 + i) >> 5;
+          start = i == 0 || ((uint32_t)__ldg(P.lists + l0 + i - 1) >> 5) != w;
+        }
+        wr += __popc(__ballot_sync(FULL, start));
+      }
+    } else {
+      wr = isect_adj<false>(P.g, tk.x, tk.y, cr, nullptr, nullptr, nullptr);
+    }
     if (INSTR) {
       const int64_t la = P.g.aoff[tk.x + 1] - P.g.aoff[tk.x], lb = P.g.aoff[tk.y + 1] - P.g.aoff[tk.y];
       inter++;
@@ -1015,6 +1190,282 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Level 1 by wedge scatter (root-grouped).  For root r, C_R1(r, s) =
+// N(r) & N(s) for every task (r, s) at once: walk the wedges r - v - s with
+// v in N(r) and s in N(v) & dir2(r) and append v to the list of task (r, s).
+// The work is the root's 2-hop pool, sum_{v in N(r)} deg(v), read as short
+// contiguous opposite-layer rows, instead of |dir2(r)| HTB intersections
+// against (possibly hub-sized) adjacency rows (htb.py:122-154).  The lists
+// are exactly the reference's C_R1 sets in ascending id order.
+//
+// Units are (root, chunk of L1_CH consecutive neighbours), one warp each,
+// drawn from an atomic queue.  dir2(r) membership and slot (= position in
+// dir2(r) = task offset from troot[r]) come from a per-warp shared-memory
+// bitmap over anchor ids plus a u16 prefix per word (n <= 65536), else from a
+// binary search of dir2(r).  Pass 1 counts hits per (unit, slot); a column
+// scan turns them into per-task list offsets and per-unit cursors; pass 2
+// appends, 32 neighbours per round, ranking same-slot hits by lane with a
+// per-warp hit mask so every list comes out sorted.
+// ---------------------------------------------------------------------------
+constexpr int L1_CH = 1024;
+constexpr int L1_THREADS = 128;
+
+struct L1Args {
+  const int64_t *__restrict__ aoff;  // anchor -> opposite
+  const int32_t *__restrict__ aidx;
+  const int64_t *__restrict__ boff;  // opposite -> anchor
+  const int32_t *__restrict__ bidx;
+  const int64_t *__restrict__ doff;  // dir2 lists (sorted ascending)
+  const int32_t *__restrict__ didx;
+  const int64_t *__restrict__ troot;
+  const int32_t *__restrict__ unit_root;
+  const int64_t *__restrict__ ubase;  // per root: aux offset of chunk 0 (stride |dir2(r)|)
+  const int32_t *__restrict__ unit_first;  // per root: first unit id
+  int64_t n_units;
+  unsigned long long *aux;  // pass 1: counts; pass 2: cursors
+  int map_words;            // bitmap words per warp (0 = binary search)
+  int shard, nshards;
+  int32_t *lists;           // pass 2
+  uint32_t *masks;          // pass 2: per-warp hit masks [mask_stride]
+  int64_t mask_stride;
+  unsigned long long *next;
+};
+
+struct RootMap {
+  uint32_t *bits;
+  uint16_t *pre;
+  const int32_t *__restrict__ d;
+  int D;
+  __device__ __forceinline__ int slot(int x) const {
+    if (bits) {
+      const uint32_t b = bits[x >> 5];
+      const int xb = x & 31;
+      if (!((b >> xb) & 1u)) return -1;
+      return pre[x >> 5] + __popc(b & ((1u << xb) - 1u));
+    }
+    int lo = 0, hi = D;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(d + mid) < x) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo < D && __ldg(d + lo) == x ? lo : -1;
+  }
+};
+
+__device__ __forceinline__ void rootmap_set(RootMap &m, bool on) {
+  if (!m.bits) return;
+  const int lane = lane_id();
+  for (int i = lane; i < m.D; i += 32) {
+    const int x = __ldg(m.d + i);
+    if (on) {
+      atomicOr(m.bits + (x >> 5), 1u << (x & 31));
+      if (i == 0 || (__ldg(m.d + i - 1) >> 5) != (x >> 5)) m.pre[x >> 5] = (uint16_t)i;
+    } else {
+      m.bits[x >> 5] = 0;
+    }
+  }
+  __syncwarp();
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
+  extern __shared__ uint32_t sm[];
+  const int lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int mw = A.map_words;
+  uint32_t *bits = mw ? sm + (int64_t)wib * (mw + (mw + 1) / 2) : nullptr;
+  uint16_t *pre = mw ? (uint16_t *)(bits + mw) : nullptr;
+  if (bits)
+    for (int i = lane; i < mw; i += 32) bits[i] = 0;
+  __syncwarp();
+  uint32_t *mask = FILL ? A.masks + gwarp * A.mask_stride : nullptr;
+  for (;;) {
+    long long u = 0;
+    if (lane == 0) u = (long long)atomicAdd(A.next, 1ull);
+    u = __shfl_sync(FULL, u, 0);
+    if (u >= A.n_units) break;
+    const int r = A.unit_root[u];
+    const int c = (int)(u - A.unit_first[r]);
+    const int64_t d0 = A.doff[r];
+    RootMap m{bits, pre, A.didx + d0, (int)(A.doff[r + 1] - d0)};
+    rootmap_set(m, true);
+    const int64_t T0 = A.troot[r];
+    unsigned long long *col = A.aux + A.ubase[r] + (int64_t)c * m.D;
+    const int64_t e0 = A.aoff[r] + (int64_t)c * L1_CH;
+    const int64_t e1 = min(A.aoff[r + 1], e0 + L1_CH);
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int64_t e = base + lane;
+      int32_t v = 0;
+      int64_t f0 = 0, f1 = 0;
+      if (e < e1) {
+        v = __ldg(A.aidx + e);
+        f0 = __ldg(A.boff + v);
+        f1 = __ldg(A.boff + v + 1);
+      }
+      if (!FILL) {
+        for (int64_t f = f0; f < f1; f++) {
+          const int k = m.slot(__ldg(A.bidx + f));
+          if (k >= 0 && (T0 + k) % A.nshards == A.shard) atomicAdd(col + k, 1ull);
+        }
+      } else {
+        // (a) hit masks, (b) ranked writes, (c) the lowest hitter advances the cursor
+        for (int64_t f = f0; f < f1; f++) {
+          const int k = m.slot(__ldg(A.bidx + f));
+          if (k >= 0 && (T0 + k) % A.nshards == A.shard) atomicOr(mask + k, 1u << lane);
+        }
+        __syncwarp();
+        for (int64_t f = f0; f < f1; f++) {
+          const int k = m.slot(__ldg(A.bidx + f));
+          if (k >= 0 && (T0 + k) % A.nshards == A.shard) {
+            const uint32_t mk = *(volatile uint32_t *)(mask + k);
+            A.lists[col[k] + __popc(mk & lanemask_lt())] = v;
+          }
+        }
+        __syncwarp();
+        for (int64_t f = f0; f < f1; f++) {
+          const int k = m.slot(__ldg(A.bidx + f));
+          if (k >= 0 && (T0 + k) % A.nshards == A.shard) {
+            const uint32_t mk = *(volatile uint32_t *)(mask + k);
+            if (mk && __ffs(mk) - 1 == lane) {
+              col[k] += __popc(mk);
+              mask[k] = 0;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();  // lanes still probing the map must finish before it is cleared
+    rootmap_set(m, false);
+  }
+}
+
+// development check: |N(r) & N(s)| by merge, thread per local task
+__global__ void l1_naive(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+                         const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
+                         const int64_t *__restrict__ cnt, unsigned long long *bad) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nloc) return;
+  const int2 tk = tasks[shard + j * nshards];
+  int64_t a = aoff[tk.x], a1 = aoff[tk.x + 1], b = aoff[tk.y], b1 = aoff[tk.y + 1], c = 0;
+  while (a < a1 && b < b1) {
+    const int x = aidx[a], y = aidx[b];
+    c += x == y;
+    a += x <= y;
+    b += y <= x;
+  }
+  if (c != cnt[j]) {
+    const unsigned long long k = atomicAdd(bad, 1ull);
+    if (k < 5) printf("l1 check: task %lld (%d,%d) naive %lld pass1 %lld\n", (long long)j, tk.x, tk.y,
+                      (long long)c, (long long)cnt[j]);
+  }
+}
+
+// per local task: |C_R1| = sum over its root's chunks (pass-1 columns)
+__global__ void l1_task_totals(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+                               const int64_t *__restrict__ troot, const int64_t *__restrict__ ubase,
+                               const int32_t *__restrict__ unit_first, const int64_t *__restrict__ doff,
+                               const unsigned long long *__restrict__ aux, int64_t *__restrict__ cnt) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nloc) return;
+  const int64_t t = shard + j * nshards;
+  const int r = tasks[t].x;
+  const int64_t k = t - troot[r], D = doff[r + 1] - doff[r];
+  const int nch = unit_first[r + 1] - unit_first[r];
+  unsigned long long c = 0;
+  for (int ch = 0; ch < nch; ch++) c += aux[ubase[r] + ch * D + k];
+  cnt[j] = (int64_t)c;
+}
+
+// per local task: pass-1 counts -> per-chunk write cursors (list offset + earlier chunks)
+__global__ void l1_cursors(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+                           const int64_t *__restrict__ troot, const int64_t *__restrict__ ubase,
+                           const int32_t *__restrict__ unit_first, const int64_t *__restrict__ doff,
+                           const int64_t *__restrict__ roff, unsigned long long *__restrict__ aux) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nloc) return;
+  const int64_t t = shard + j * nshards;
+  const int r = tasks[t].x;
+  const int64_t k = t - troot[r], D = doff[r + 1] - doff[r];
+  const int nch = unit_first[r + 1] - unit_first[r];
+  unsigned long long run = (unsigned long long)roff[j];
+  for (int ch = 0; ch < nch; ch++) {
+    unsigned long long *p = aux + ubase[r] + ch * D + k;
+    const unsigned long long x = *p;
+    *p = run;
+    run += x;
+  }
+}
+
+// per root: chunks (units) and aux block size (0 for roots without tasks)
+__global__ void l1_root_sizes(const int64_t *__restrict__ aoff, const int64_t *__restrict__ doff,
+                              const int64_t *__restrict__ troot, int64_t n, int32_t *__restrict__ nunits,
+                              int64_t *__restrict__ auxw) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int32_t nu = 0;
+  int64_t w = 0;
+  const int64_t D = doff[r + 1] - doff[r];
+  if (troot[r] >= 0 && D > 0) {
+    const int64_t deg = aoff[r + 1] - aoff[r];
+    nu = (int32_t)((deg + L1_CH - 1) / L1_CH);
+    w = (int64_t)nu * D;
+  }
+  nunits[r] = nu;
+  auxw[r] = w;
+}
+
+__global__ void l1_unit_roots(const int32_t *__restrict__ unit_first, int64_t n,
+                              int32_t *__restrict__ unit_root) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int32_t u = unit_first[r]; u < unit_first[r + 1]; u++) unit_root[u] = (int32_t)r;
+}
+
+__global__ void max_dir_len(const int64_t *__restrict__ doff, int64_t n, unsigned long long *out) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long v = r < n ? (unsigned long long)(doff[r + 1] - doff[r]) : 0ull;
+  v = __reduce_max_sync(FULL, (unsigned)v);
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
+// probe-cost estimate of level 1 (sum over local tasks of the shorter adjacency
+// slice) vs the wedge pool of the roots: decides the level-1 mode
+__global__ void l1_probe_cost(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+                             const int64_t *__restrict__ hoff, unsigned long long *out) {
+  unsigned long long c = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nloc;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int2 tk = tasks[shard + j * nshards];
+    const int64_t a = hoff[tk.x + 1] - hoff[tk.x], b = hoff[tk.y + 1] - hoff[tk.y];
+    c += (unsigned long long)(a < b ? a : b);
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void l1_pool(const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
+                        const int64_t *__restrict__ boff, const int64_t *__restrict__ troot,
+                        int64_t n, unsigned long long *out) {
+  // warp per root with tasks: sum of its neighbours' degrees
+  const int lane = lane_id();
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long c = 0;
+  for (int64_t r = gw; r < n; r += nw) {
+    if (troot[r] < 0) continue;
+    for (int64_t e = aoff[r] + lane; e < aoff[r + 1]; e += 32) {
+      const int v = aidx[e];
+      c += (unsigned long long)(boff[v + 1] - boff[v]);
+    }
+  }
+  c = warp_sum(c);
+  if (lane == 0 && c) atomicAdd(out, c);
+}
+
+// ---------------------------------------------------------------------------
 // enumeration (engine.py:315-374) over the task-local universe
 // ---------------------------------------------------------------------------
 struct EnumArgs {
@@ -1028,6 +1479,8 @@ struct EnumArgs {
   const int64_t *frame_off;           // SPLIT: [q1 - q0]
   SplitSink sink;
   const unsigned long long *sub_order;  // sub_kernel: record offsets, LPT order
+  int triage;                           // > 0: defer tasks with more level-1 R-survivors
+  int32_t *heavy;                       //   (or a frame over the scratch) to heavy[]
 };
 
 __device__ __forceinline__ void finish_task(const Params &P, Acc128 acc, int64_t t, bool atomic,
@@ -1108,8 +1561,9 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
     const int2 tk = P.tasks[t];
     const Dims d = dims_of(A.info[j]);
     const bool rowL = SPLIT || has_rowL(p_eff, P.map_words);
-    const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, rowL, INSTR);
-    const int64_t sc = scratch_words(d.nR, d.nL, p_eff);
+    const int cap = SPLIT ? 0 : A.triage;
+    const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, rowL, INSTR, cap);
+    const int64_t sc = scratch_words(d.nR, d.nL, p_eff, cap);
     uint32_t *ro_base, *sc_base;
     if (SPLIT) {
       ro_base = A.frames + A.frame_off[qi - A.q0];
@@ -1124,13 +1578,24 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
       spills++;
     }
     if (!sc_base || (sc_base == my_global && (SPLIT ? sc : ro + sc) > A.gscratch_words)) {
-      if (lane == 0) atomicExch(P.overflow, 2);  // cannot happen: sized from level-1 maxima
+      if (A.triage > 0 && !SPLIT) {  // frame too large for the scratch: the split path takes it
+        if (lane == 0) A.heavy[atomicAdd(P.ctr + CTR_HEAVY, 1ull)] = j;
+        __syncwarp();
+      } else if (lane == 0) {
+        atomicExch(P.overflow, 2);  // cannot happen: sized from level-1 maxima
+      }
       continue;
     }
     Frame f;
-    carve_ro(f, ro_base, d, rowL, INSTR);
-    carve_scratch(f, sc_base, d, p_eff);
-    build_frame<INSTR, LAZY>(P, f, d, tk.x, tk.y, map, ph_);
+    carve_ro(f, ro_base, d, rowL, INSTR, cap);
+    carve_scratch(f, sc_base, d, p_eff, cap);
+    const int ns1 = build_frame_R<INSTR>(P, f, d, tk.x, tk.y, j, map, ph_);
+    if (!SPLIT && A.triage > 0 && ns1 > A.triage) {  // heavy: defer to the split path
+      if (lane == 0) A.heavy[atomicAdd(P.ctr + CTR_HEAVY, 1ull)] = j;
+      clear_map(map, f, d);
+      continue;
+    }
+    build_frame_L<INSTR, LAZY>(P, f, d, map, rowL, ph_);
     init_root_sets(f, d);
     Acc128 acc{0, 0};
     if (SPLIT) {
@@ -1199,6 +1664,11 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
   }
   PH_FLUSH();
   flush_tallies(P, total, tl, 0, spills, INSTR);
+}
+
+__global__ void gather_keys(const int32_t *ids, int64_t n, const uint32_t *cost, uint32_t *out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = cost[ids[i]];
 }
 
 __global__ void iota32(int32_t *a, int64_t n) {
@@ -1273,6 +1743,26 @@ T sum_device(const T *p, int64_t n, cudaStream_t st) {
   return h;
 }
 
+// BC_DEBUG=1: synchronising stage timer on stderr (development only)
+struct DbgTimer {
+  bool on;
+  cudaStream_t st;
+  double t0;
+  explicit DbgTimer(cudaStream_t s) : on(getenv("BC_DEBUG") != nullptr), st(s), t0(now()) {}
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+  }
+  void mark(const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const double t = now();
+    fprintf(stderr, "[bc search] %-14s %9.3f ms\n", what, 1e3 * (t - t0));
+    t0 = t;
+  }
+};
+
 int env_int(const char *name, int dflt) {  // development knobs
   const char *v = getenv(name);
   return v && *v ? atoi(v) : dflt;
@@ -1344,7 +1834,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   }
   Params P;
   P.g = Graph2{s.hadj_off.p, s.hadj_idx.p, s.hadj_val.p, s.hdir_off.p, s.hdir_idx.p, s.hdir_val.p,
-               s.dense_id.p, s.dense.p, s.dense_mw};
+               s.dense_id.p, s.dense.p, s.dense_mw, s.boff, s.bidx};
   P.tasks = s.tasks.p;
   P.n_tasks = n_tasks;
   P.shard = shard;
@@ -1359,6 +1849,9 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.overflow = ovf.p;
   P.ctr = ctr.p;
   P.task_counts = want_tc ? tcounts.p : nullptr;
+  P.roff = nullptr;
+  P.lists = nullptr;
+  P.rowR_mode = (cfg.flags & BC_FLAG_ROWR_SCATTER) ? 1 : (cfg.flags & BC_FLAG_ROWR_PROBE) ? 2 : 0;
   // slot map over anchor words for rowL (u16 per word) when it is small
   const int64_t anchor_words = (s.n + 31) / 32;
   P.map_words = (s.p_eff >= 4 && anchor_words <= 4096) ? (int)((anchor_words + 1) & ~1) : 0;
@@ -1381,12 +1874,146 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     DBuf<uint32_t> cost;
     info.alloc(nloc, st);
     cost.alloc(nloc, st);
+    // ---- level-1 mode: wedge scatter (root-grouped C_R1 lists) when the roots'
+    // 2-hop pools cost less than the per-task probes of the shorter adjacency slice
+    DBuf<int64_t> l1_roff;
+    DBuf<int32_t> l1_lists;
+    int l1_mode = (cfg.flags & BC_FLAG_L1_SCATTER) ? 1 : (cfg.flags & BC_FLAG_L1_PROBE) ? 2 : 0;
+    if (l1_mode == 0) {
+      DBuf<unsigned long long> c2;
+      c2.alloc(2, st);
+      c2.zero();
+      l1_probe_cost<<<sms * 8, 256, 0, st>>>(s.tasks.p, nloc, shard, nshards, s.hadj_off.p, c2.p);
+      l1_pool<<<sms * 8, 256, 0, st>>>(s.aoff, s.aidx, s.boff, s.troot.p, s.n, c2.p + 1);
+      BC_CHECK_LAUNCH();
+      unsigned long long hc[2];
+      copy_d2h(hc, c2.p, sizeof hc, st);
+      BC_CUDA(cudaStreamSynchronize(st));
+      launches += 2;
+      // a probe is a bisect step chain (~4x a streamed id); the scatter walks each
+      // pool ~4 times (count, mask, write, cursor)
+      l1_mode = 4.0 * (double)hc[1] < 4.0 * (double)hc[0] ? 1 : 2;
+      if (getenv("BC_DEBUG"))
+        fprintf(stderr, "[bc level1] probe words %llu  pool %llu  -> %s\n", hc[0], hc[1],
+                l1_mode == 1 ? "scatter" : "probe");
+    }
+    DbgTimer dt(st);
+    if (l1_mode == 1) {
+      const int64_t n = s.n;
+      DBuf<int32_t> nunits, unit_first, unit_root;
+      DBuf<int64_t> auxw, ubase;
+      nunits.alloc(n + 1, st);
+      auxw.alloc(n + 1, st);
+      nunits.zero();
+      auxw.zero();
+      l1_root_sizes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.aoff, s.dir_off.p, s.troot.p, n,
+                                                                 nunits.p, auxw.p);
+      unit_first.alloc(n + 1, st);
+      ubase.alloc(n + 1, st);
+      scan_excl(nunits.p, unit_first.p, n + 1, st);
+      scan_excl(auxw.p, ubase.p, n + 1, st);
+      DBuf<unsigned long long> mx;
+      mx.alloc(1, st);
+      mx.zero();
+      max_dir_len<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.dir_off.p, n, mx.p);
+      int32_t n_units = 0;
+      int64_t aux_total = 0;
+      unsigned long long maxD = 0;
+      copy_d2h(&n_units, unit_first.p + n, sizeof n_units, st);
+      copy_d2h(&aux_total, ubase.p + n, sizeof aux_total, st);
+      copy_d2h(&maxD, mx.p, sizeof maxD, st);
+      BC_CUDA(cudaStreamSynchronize(st));
+      unit_root.alloc(n_units, st);
+      l1_unit_roots<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(unit_first.p, n, unit_root.p);
+      DBuf<unsigned long long> aux, nxt;
+      aux.alloc(aux_total, st);
+      aux.zero();
+      nxt.alloc(2, st);
+      nxt.zero();
+      L1Args A1{};
+      A1.aoff = s.aoff;
+      A1.aidx = s.aidx;
+      A1.boff = s.boff;
+      A1.bidx = s.bidx;
+      A1.doff = s.dir_off.p;
+      A1.didx = s.dir_idx.p;
+      A1.troot = s.troot.p;
+      A1.unit_root = unit_root.p;
+      A1.ubase = ubase.p;
+      A1.unit_first = unit_first.p;
+      A1.n_units = n_units;
+      A1.aux = aux.p;
+      A1.map_words = n <= 65536 ? (int)((n + 31) / 32) : 0;
+      A1.shard = shard;
+      A1.nshards = nshards;
+      A1.next = nxt.p;
+      const int l1w = L1_THREADS / 32;
+      const size_t l1smem = (size_t)l1w * (A1.map_words + (A1.map_words + 1) / 2) * 4;
+      int per_sm = 0;
+      BC_CUDA(cudaFuncSetAttribute(l1_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)l1smem));
+      BC_CUDA(cudaFuncSetAttribute(l1_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)l1smem));
+      BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l1_scatter<true>, L1_THREADS,
+                                                            l1smem));
+      const int64_t l1blocks = (int64_t)sms * std::max(per_sm, 1);
+      dt.mark("l1 setup");
+      l1_scatter<false><<<(unsigned)l1blocks, L1_THREADS, l1smem, st>>>(A1);
+      BC_CHECK_LAUNCH();
+      dt.mark("l1 count");
+      DBuf<int64_t> cnt;
+      cnt.alloc(nloc + 1, st);
+      cnt.zero();
+      l1_task_totals<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
+          s.tasks.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p, s.dir_off.p, aux.p,
+          cnt.p);
+      if (getenv("BC_CHECK_L1")) {
+        DBuf<unsigned long long> bad;
+        bad.alloc(1, st);
+        bad.zero();
+        l1_naive<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(s.tasks.p, nloc, shard, nshards,
+                                                                 s.aoff, s.aidx, cnt.p, bad.p);
+        unsigned long long hb = 0;
+        copy_d2h(&hb, bad.p, 8, st);
+        BC_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[bc level1] check: %llu of %lld task counts differ\n", hb, (long long)nloc);
+      }
+      l1_roff.alloc(nloc + 1, st);
+      scan_excl(cnt.p, l1_roff.p, nloc + 1, st);
+      int64_t n_entries = 0;
+      copy_d2h(&n_entries, l1_roff.p + nloc, sizeof n_entries, st);
+      BC_CUDA(cudaStreamSynchronize(st));
+      l1_lists.alloc(n_entries, st);
+      l1_cursors<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
+          s.tasks.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p, s.dir_off.p,
+          l1_roff.p, aux.p);
+      DBuf<uint32_t> masks;
+      A1.mask_stride = (int64_t)std::max<unsigned long long>(maxD, 1);
+      masks.alloc((size_t)l1blocks * l1w * A1.mask_stride, st);
+      masks.zero();
+      A1.masks = masks.p;
+      A1.lists = l1_lists.p;
+      A1.next = nxt.p + 1;
+      dt.mark("l1 offsets");
+      l1_scatter<true><<<(unsigned)l1blocks, L1_THREADS, l1smem, st>>>(A1);
+      BC_CHECK_LAUNCH();
+      dt.mark("l1 fill");
+      launches += 12;
+      P.roff = l1_roff.p;
+      P.lists = l1_lists.p;
+      if (getenv("BC_DEBUG")) {
+        BC_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[bc level1] scatter: %d units, %lld aux, %lld C_R1 entries\n", n_units,
+                (long long)aux_total, (long long)n_entries);
+      }
+    }
     {
       int64_t blocks = (nloc * 32 + 255) / 256;
       blocks = std::min<int64_t>(blocks, (int64_t)sms * 32);
       if (instr) level1_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
       else level1_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
       BC_CHECK_LAUNCH();
+      dt.mark("level1_kernel");
       launches++;
     }
     BC_CUDA(cudaEventRecord(e1, st));
@@ -1396,6 +2023,63 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       BC_CUDA(cudaStreamSynchronize(st));
       n_alive = (int64_t)h[CTR_ALIVE];
       const int64_t max_ro = (int64_t)h[CTR_MAXRO], max_scr = (int64_t)h[CTR_MAXSCR];
+      if (const char *dump = getenv("BC_DUMP_L1")) {  // development: Info + C_R1 lists
+        std::vector<Info> hi(nloc);
+        copy_d2h(hi.data(), info.p, nloc * sizeof(Info), st);
+        std::vector<int64_t> ro;
+        std::vector<int32_t> li;
+        if (P.lists) {
+          ro.resize(nloc + 1);
+          copy_d2h(ro.data(), P.roff, (nloc + 1) * 8, st);
+          BC_CUDA(cudaStreamSynchronize(st));
+          li.resize(ro[nloc]);
+          copy_d2h(li.data(), P.lists, ro[nloc] * 4, st);
+        }
+        BC_CUDA(cudaStreamSynchronize(st));
+        if (FILE *fh = fopen(dump, "wb")) {
+          int64_t n = nloc, nl = (int64_t)li.size();
+          fwrite(&n, 8, 1, fh);
+          fwrite(hi.data(), sizeof(Info), nloc, fh);
+          fwrite(&nl, 8, 1, fh);
+          if (nl) {
+            fwrite(ro.data(), 8, nloc + 1, fh);
+            fwrite(li.data(), 4, nl, fh);
+          }
+          fclose(fh);
+        }
+      }
+      if (getenv("BC_LEVEL1_STATS")) {  // development: level-1 shape of the workload
+        std::vector<Info> hi(nloc);
+        copy_d2h(hi.data(), info.p, nloc * sizeof(Info), st);
+        BC_CUDA(cudaStreamSynchronize(st));
+        std::vector<int> crs, cls;
+        double sum_lr = 0, sum_rowR = 0;
+        for (const Info &x : hi)
+          if (x.cl >= s.p_eff - 2 && x.cr >= s.q_eff) {
+            crs.push_back(x.cr);
+            cls.push_back(x.cl);
+            sum_lr += (double)x.cl * x.cr;
+            sum_rowR += (double)x.cl * ((x.cr + 31) / 32);
+          }
+        std::sort(crs.begin(), crs.end());
+        std::sort(cls.begin(), cls.end());
+        auto pct = [](const std::vector<int> &v, double f) {
+          return v.empty() ? 0 : v[std::min(v.size() - 1, (size_t)(f * v.size()))];
+        };
+        float l1ms = 0;
+        BC_CUDA(cudaEventRecord(e1, st));
+        BC_CUDA(cudaEventSynchronize(e1));
+        BC_CUDA(cudaEventElapsedTime(&l1ms, e0, e1));
+        fprintf(stderr,
+                "[bc level1] tasks %lld alive %lld  level1 %.3f ms  max_ro %lld max_scr %lld words\n"
+                "  |C_R1| p50 %d p90 %d p99 %d max %d   |C_L1| p50 %d p90 %d p99 %d max %d\n"
+                "  sum |C_L1||C_R1| %.4g  sum rowR words %.4g\n",
+                (long long)nloc, (long long)n_alive, l1ms, (long long)max_ro, (long long)max_scr,
+                pct(crs, .5), pct(crs, .9), pct(crs, .99), crs.empty() ? 0 : crs.back(),
+                pct(cls, .5), pct(cls, .9), pct(cls, .99), cls.empty() ? 0 : cls.back(), sum_lr,
+                sum_rowR);
+        if (getenv("BC_LEVEL1_ONLY")) n_alive = 0;
+      }
       if (n_alive > 0) {
         // pre-runtime LPT order: alive tasks by |C_L1|*|C_R1| descending
         DBuf<int32_t> ids, queue;
@@ -1431,110 +2115,166 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           BC_CHECK_LAUNCH();
           launches++;
         } else {
-          // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
-          // writes every frame to the frame arena and pushes the split-level nodes,
-          // then sub_kernel drains them heaviest first with every warp.
-          const int split_level = s.p_eff <= 6 ? 2 : 3;
-          const int budget = env_int("BC_SPLIT_BUDGET", 1024);
-          const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
-          auto kern = instr ? enum_kernel<true, false, true> : enum_kernel<false, false, true>;
-          auto sk = instr ? sub_kernel<true> : sub_kernel<false>;
-          const size_t ssmem = (size_t)wpb * (budget + LEAF_WORDS) * 4;
-          const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
-          const int64_t sblocks = std::min<int64_t>((int64_t)sms * blocks_per_sm(sk, ssmem), blocks);
-          A.budget_words = budget;
-          DBuf<uint32_t> gs;
-          if (max_scr > budget) {
-            A.gscratch_words = (max_scr + 31) & ~int64_t(31);
-            gs.alloc((size_t)blocks * wpb * A.gscratch_words, st);
-            A.gscratch = gs.p;
-          }
-          const int64_t arena_limit = int64_t(1) << 28;  // words per arena (1 GiB)
-          DBuf<int64_t> ro, sub, foff, soff;
-          ro.alloc(n_alive + 1, st);
-          sub.alloc(n_alive + 1, st);
-          foff.alloc(n_alive + 1, st);
-          soff.alloc(n_alive + 1, st);
-          ro.zero();
-          sub.zero();
-          split_sizes<<<(unsigned)((n_alive + 255) / 256), 256, 0, st>>>(
-              info.p, queue.p, 0, n_alive, instr, split_level, ro.p, sub.p);
-          scan_excl(ro.p, foff.p, n_alive + 1, st);
-          scan_excl(sub.p, soff.p, n_alive + 1, st);
-          std::vector<int64_t> hf(n_alive + 1), hs(n_alive + 1);
-          copy_d2h(hf.data(), foff.p, (n_alive + 1) * 8, st);
-          copy_d2h(hs.data(), soff.p, (n_alive + 1) * 8, st);
-          BC_CUDA(cudaStreamSynchronize(st));
-          launches += 3;
-          int64_t q0 = 0;
-          while (q0 < n_alive) {
-            // grow the chunk while both arenas stay under the limit
-            int64_t q1 = q0 + 1;
-            {
-              int64_t lo = q0 + 1, hi = n_alive;
-              while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) / 2;
-                if (hf[mid] - hf[q0] <= arena_limit && hs[mid] - hs[q0] <= arena_limit) lo = mid;
-                else hi = mid - 1;
-              }
-              q1 = lo;
-            }
-            const int64_t fw = hf[q1] - hf[q0];
-            const int64_t sw = std::max<int64_t>(hs[q1] - hs[q0], 8);
-            DBuf<uint32_t> frames, arena;
-            DBuf<unsigned long long> index;
-            DBuf<int64_t> local_off;
-            frames.alloc(fw, st);
-            arena.alloc(sw, st);
-            const int64_t cap = sw / 6 + 1;
-            index.alloc(cap, st);
-            local_off.alloc(q1 - q0, st);
-            // frame offsets relative to the chunk
-            {
-              std::vector<int64_t> lo_off(q1 - q0);
-              for (int64_t i = q0; i < q1; i++) lo_off[i - q0] = hf[i] - hf[q0];
-              copy_h2d(local_off.p, lo_off.data(), (q1 - q0) * 8, st);
+          // triage (p_eff >= 5): every task is started whole by one warp; a task with
+          // at most T level-1 R-survivors (whose frame fits the scratch) finishes in
+          // place, the rest are deferred, heaviest first, to the split path below.
+          int64_t n_heavy = n_alive;
+          const int32_t *hq_p = queue.p;
+          DBuf<int32_t> heavy, hq;
+          const int T = env_int("BC_TRIAGE", 32);
+          if (T > 0) {
+            const int budget = env_int("BC_TRIAGE_BUDGET", 1536);
+            const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
+            auto kern = instr ? enum_kernel<true, false, false> : enum_kernel<false, false, false>;
+            const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
+            heavy.alloc(n_alive, st);
+            EnumArgs B = A;
+            B.q0 = 0;
+            B.q1 = n_alive;
+            B.budget_words = budget;
+            B.triage = T;
+            B.heavy = heavy.p;
+            DBuf<uint32_t> gs;
+            if (max_ro + max_scr > budget) {
+              // per-warp frame scratch, capped at 4 GiB in total (larger frames defer)
+              int64_t w = (max_ro + max_scr + 31) & ~int64_t(31);
+              const int64_t cap_w = ((int64_t(1) << 30) / (blocks * wpb)) & ~int64_t(31);
+              B.gscratch_words = std::min(w, cap_w);
+              gs.alloc((size_t)blocks * wpb * B.gscratch_words, st);
+              B.gscratch = gs.p;
             }
             BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
-            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_USED, 0, 8, st));
-            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_N, 0, 8, st));
-            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_NEXT, 0, 8, st));
-            A.q0 = q0;
-            A.q1 = q1;
-            A.frames = frames.p;
-            A.frame_off = local_off.p;
-            A.sink.arena = arena.p;
-            A.sink.arena_words = sw;
-            A.sink.index = index.p;
-            A.sink.index_cap = cap;
-            A.sink.level = split_level;
-            kern<<<(unsigned)blocks, ENUM_THREADS, smem, st>>>(P, A);
+            dt.mark("pre-triage");
+            kern<<<(unsigned)blocks, ENUM_THREADS, smem, st>>>(P, B);
             BC_CHECK_LAUNCH();
+            dt.mark("triage");
+            launches++;
             unsigned long long hn = 0;
-            copy_d2h(&hn, ctr.p + CTR_SUB_N, sizeof hn, st);
+            copy_d2h(&hn, ctr.p + CTR_HEAVY, sizeof hn, st);
             BC_CUDA(cudaStreamSynchronize(st));
-            const int64_t n_sub = std::min<int64_t>((int64_t)hn, cap);
-            launches += 1;
-            if (n_sub > 0) {
-              DBuf<uint32_t> k0, k1;
-              DBuf<unsigned long long> v1;
-              k0.alloc(n_sub, st);
-              k1.alloc(n_sub, st);
-              DBuf<unsigned long long> v0;
-              v0.alloc(n_sub, st);
-              v1.alloc(n_sub, st);
-              sub_keys<<<(unsigned)((n_sub + 255) / 256), 256, 0, st>>>(arena.p, index.p, n_sub,
-                                                                      info.p, k0.p, v0.p);
-              sort_pairs_desc(k0.p, k1.p, v0.p, v1.p, n_sub, st);
-              A.sub_order = v1.p;
-              sk<<<(unsigned)sblocks, ENUM_THREADS, ssmem, st>>>(P, A, n_sub);
-              BC_CHECK_LAUNCH();
-              launches += 3;
+            n_heavy = (int64_t)hn;
+            if (n_heavy > 0) {  // deferred tasks in LPT order again (deterministic)
+              DBuf<uint32_t> hk, hk2;
+              hk.alloc(n_heavy, st);
+              hk2.alloc(n_heavy, st);
+              hq.alloc(n_heavy, st);
+              gather_keys<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(heavy.p, n_heavy,
+                                                                              cost.p, hk.p);
+              sort_pairs_desc(hk.p, hk2.p, heavy.p, hq.p, n_heavy, st);
+              launches += 2;
             }
-            n_sub_total += n_sub;
-            q0 = q1;
+            hq_p = hq.p;
           }
-          n_split = n_alive;
+          A.queue = hq_p;
+          if (n_heavy > 0) {
+          // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
+            // writes every frame to the frame arena and pushes the split-level nodes,
+            // then sub_kernel drains them heaviest first with every warp.
+            const int split_level = s.p_eff <= 6 ? 2 : 3;
+            const int budget = env_int("BC_SPLIT_BUDGET", 1024);
+            const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
+            auto kern = instr ? enum_kernel<true, false, true> : enum_kernel<false, false, true>;
+            auto sk = instr ? sub_kernel<true> : sub_kernel<false>;
+            const size_t ssmem = (size_t)wpb * (budget + LEAF_WORDS) * 4;
+            const int64_t blocks = (int64_t)sms * blocks_per_sm(kern, smem);
+            const int64_t sblocks = std::min<int64_t>((int64_t)sms * blocks_per_sm(sk, ssmem), blocks);
+            A.budget_words = budget;
+            DBuf<uint32_t> gs;
+            if (max_scr > budget) {
+              A.gscratch_words = (max_scr + 31) & ~int64_t(31);
+              gs.alloc((size_t)blocks * wpb * A.gscratch_words, st);
+              A.gscratch = gs.p;
+            }
+            const int64_t arena_limit = int64_t(1) << 28;  // words per arena (1 GiB)
+            DBuf<int64_t> ro, sub, foff, soff;
+            ro.alloc(n_heavy + 1, st);
+            sub.alloc(n_heavy + 1, st);
+            foff.alloc(n_heavy + 1, st);
+            soff.alloc(n_heavy + 1, st);
+            ro.zero();
+            sub.zero();
+            split_sizes<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(
+                info.p, hq_p, 0, n_heavy, instr, split_level, ro.p, sub.p);
+            scan_excl(ro.p, foff.p, n_heavy + 1, st);
+            scan_excl(sub.p, soff.p, n_heavy + 1, st);
+            std::vector<int64_t> hf(n_heavy + 1), hs(n_heavy + 1);
+            copy_d2h(hf.data(), foff.p, (n_heavy + 1) * 8, st);
+            copy_d2h(hs.data(), soff.p, (n_heavy + 1) * 8, st);
+            BC_CUDA(cudaStreamSynchronize(st));
+            launches += 3;
+            int64_t q0 = 0;
+            while (q0 < n_heavy) {
+              // grow the chunk while both arenas stay under the limit
+              int64_t q1 = q0 + 1;
+              {
+                int64_t lo = q0 + 1, hi = n_heavy;
+                while (lo < hi) {
+                  const int64_t mid = (lo + hi + 1) / 2;
+                  if (hf[mid] - hf[q0] <= arena_limit && hs[mid] - hs[q0] <= arena_limit) lo = mid;
+                  else hi = mid - 1;
+                }
+                q1 = lo;
+              }
+              const int64_t fw = hf[q1] - hf[q0];
+              const int64_t sw = std::max<int64_t>(hs[q1] - hs[q0], 8);
+              DBuf<uint32_t> frames, arena;
+              DBuf<unsigned long long> index;
+              DBuf<int64_t> local_off;
+              frames.alloc(fw, st);
+              arena.alloc(sw, st);
+              const int64_t cap = sw / 6 + 1;
+              index.alloc(cap, st);
+              local_off.alloc(q1 - q0, st);
+              // frame offsets relative to the chunk
+              {
+                std::vector<int64_t> lo_off(q1 - q0);
+                for (int64_t i = q0; i < q1; i++) lo_off[i - q0] = hf[i] - hf[q0];
+                copy_h2d(local_off.p, lo_off.data(), (q1 - q0) * 8, st);
+              }
+              BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
+              BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_USED, 0, 8, st));
+              BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_N, 0, 8, st));
+              BC_CUDA(cudaMemsetAsync(ctr.p + CTR_SUB_NEXT, 0, 8, st));
+              A.q0 = q0;
+              A.q1 = q1;
+              A.frames = frames.p;
+              A.frame_off = local_off.p;
+              A.sink.arena = arena.p;
+              A.sink.arena_words = sw;
+              A.sink.index = index.p;
+              A.sink.index_cap = cap;
+              A.sink.level = split_level;
+              kern<<<(unsigned)blocks, ENUM_THREADS, smem, st>>>(P, A);
+              BC_CHECK_LAUNCH();
+              unsigned long long hn = 0;
+              copy_d2h(&hn, ctr.p + CTR_SUB_N, sizeof hn, st);
+              BC_CUDA(cudaStreamSynchronize(st));
+              const int64_t n_sub = std::min<int64_t>((int64_t)hn, cap);
+              launches += 1;
+              if (n_sub > 0) {
+                DBuf<uint32_t> k0, k1;
+                DBuf<unsigned long long> v1;
+                k0.alloc(n_sub, st);
+                k1.alloc(n_sub, st);
+                DBuf<unsigned long long> v0;
+                v0.alloc(n_sub, st);
+                v1.alloc(n_sub, st);
+                sub_keys<<<(unsigned)((n_sub + 255) / 256), 256, 0, st>>>(arena.p, index.p, n_sub,
+                                                                        info.p, k0.p, v0.p);
+                sort_pairs_desc(k0.p, k1.p, v0.p, v1.p, n_sub, st);
+                A.sub_order = v1.p;
+                sk<<<(unsigned)sblocks, ENUM_THREADS, ssmem, st>>>(P, A, n_sub);
+                BC_CHECK_LAUNCH();
+                launches += 3;
+              }
+              n_sub_total += n_sub;
+              q0 = q1;
+            }
+          }
+          dt.mark("split");
+          if (dt.on) fprintf(stderr, "[bc search] alive %lld heavy %lld\n", (long long)n_alive,
+                             (long long)n_heavy);
+          n_split = n_heavy;
         }
       }
     }

@@ -29,6 +29,7 @@ from .graph import BipartiteGraph, CsrView, as_csr
 MODES = ("dfs", "hybrid")
 ANCHOR_FLAGS = ("auto", "U", "V")
 ORDER_MODES = ("reference",)
+KERNEL_CHOICES = ("auto", "scatter", "probe")
 
 
 @dataclass
@@ -44,6 +45,8 @@ class EngineConfig:
     device: int = 0
     order_mode: str = "reference"
     instrument: bool = False  # tally reference-equivalent intersections (B_enum)
+    level1: str = "auto"      # "scatter" (root-grouped wedge walk) | "probe" (per-task HTB)
+    rows: str = "auto"        # candidate rows: "scatter" | "probe"
 
     def validate(self) -> None:
         if self.worker_count < 1:
@@ -56,6 +59,8 @@ class EngineConfig:
             raise ValueError(f"anchor must be one of {ANCHOR_FLAGS}")
         if self.order_mode not in ORDER_MODES:
             raise ValueError(f"order_mode must be one of {ORDER_MODES}")
+        if self.level1 not in KERNEL_CHOICES or self.rows not in KERNEL_CHOICES:
+            raise ValueError(f"level1 / rows must be one of {KERNEL_CHOICES}")
         if self.enumerate_results:
             raise NotImplementedError(
                 "enumerate_results is not provided by the B200 counting path "
@@ -153,6 +158,9 @@ def _make_config(cfg: EngineConfig, anchor: str, rank, roots, shard=(0, 1), flag
     c.device = int(cfg.device)
     c.shard_index, c.shard_count = int(shard[0]), int(shard[1])
     c.flags = flags | (_abi.BC_FLAG_INSTRUMENT if cfg.instrument else 0)
+    c.flags |= {"auto": 0, "scatter": _abi.BC_FLAG_L1_SCATTER, "probe": _abi.BC_FLAG_L1_PROBE}[cfg.level1]
+    c.flags |= {"auto": 0, "scatter": _abi.BC_FLAG_ROWR_SCATTER,
+                "probe": _abi.BC_FLAG_ROWR_PROBE}[cfg.rows]
     keep = []
     if rank is not None:
         r = np.ascontiguousarray(rank, dtype=np.int64)
@@ -186,6 +194,26 @@ class DeviceGraph:
         self._h = h
         self.device = device
         self.u_count, self.v_count = nu, nv
+
+    @classmethod
+    def from_device_csr(cls, u_off, u_idx, v_off, v_idx, device: int = 0) -> "DeviceGraph":
+        """Adopt a CSR already in HBM (torch CUDA tensors: int64 offsets, int32
+        ids), e.g. ``synth.fr_shaped_csr(device="cuda")``; copied device to device."""
+        L = _abi.load()
+        ts = [u_off, u_idx, v_off, v_idx]
+        for t, dt in zip(ts, ("int64", "int32", "int64", "int32")):
+            if not t.is_cuda or str(t.dtype) != f"torch.{dt}" or not t.is_contiguous():
+                raise ValueError("device CSR must be contiguous CUDA tensors (int64 off, int32 idx)")
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        nu, nv = u_off.numel() - 1, v_off.numel() - 1
+        _abi.check(L.bc_graph_create_device(u_off.data_ptr(), u_idx.data_ptr(), nu,
+                                            v_off.data_ptr(), v_idx.data_ptr(), nv, device,
+                                            C.byref(h)))
+        self._h = h
+        self.device = device
+        self.u_count, self.v_count = nu, nv
+        return self
 
     def count_raw(self, p: int, q: int, cfg: EngineConfig | None = None, *, anchor=None,
                   rank=None, roots=None, shard=(0, 1), task_counts: bool = False):

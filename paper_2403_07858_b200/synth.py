@@ -207,6 +207,114 @@ def fr_shaped(nu: int = 44_000, nv: int = 8_956_000, m: int = 100_000_000,
     return csr_from_sorted_keys(nu, nv, key)
 
 
+def _s64(x: int) -> int:
+    """Unsigned 64-bit constant as a signed int64 value (two's complement)."""
+    return x - (1 << 64) if x >= 1 << 63 else x
+
+
+_SM_GAMMA, _SM_M1, _SM_M2 = _s64(0x9E3779B97F4A7C15), _s64(0xBF58476D1CE4E5B9), _s64(0x94D049BB133111EB)
+
+
+def _lsr(x, s: int):
+    """Logical right shift of an int64 torch tensor."""
+    return (x >> s) & ((1 << (64 - s)) - 1)
+
+
+def splitmix64(x):
+    """SplitMix64 finaliser on int64 torch tensors (wrapping arithmetic): a
+    counter-based hash, so the stream is identical on CPU and GPU and for any
+    chunking of the counter range."""
+    z = x + _SM_GAMMA
+    z = (z ^ _lsr(z, 30)) * _SM_M1
+    z = (z ^ _lsr(z, 27)) * _SM_M2
+    return z ^ _lsr(z, 31)
+
+
+def _capped_cdf(n: int, gamma: float, cap: float, m: int, scale_bits: int = 40) -> np.ndarray:
+    """Integer cumulative Chung-Lu weights (i+1)^(-1/(gamma-1)), clipped at
+    cap/m and renormalised 30 times, in fixed point so the
+    inverse-CDF sampling below is exact integer arithmetic on any device."""
+    w = (np.arange(n) + 1.0) ** (-1.0 / (gamma - 1.0))
+    w /= w.sum()
+    lim = cap / m
+    for _ in range(30):
+        w = np.minimum(w, lim)
+        w /= w.sum()
+    wi = np.maximum(np.floor(w * float(1 << scale_bits)), 1).astype(np.int64)
+    return np.cumsum(wi)
+
+
+def fr_shaped_csr(nu: int = 44_000, nv: int = 8_956_000, m: int = 100_000_000,
+                  gamma_u: float = 2.5, gamma_v: float = 2.5, cap_u: float = 200_000,
+                  cap_v: float = 64, seed: int = 5, n_cores: int = 64, core_seed: int = 9,
+                  device=None, chunk: int = 1 << 25):
+    """C5 built directly as device CSR (both views), FR-shaped:
+    a small dense U (44K) against a huge sparse V (8.956M), capped Chung-Lu
+    degrees, plus ``n_cores`` copies of C4's three planted core shapes.
+
+    Endpoint draws are SplitMix64(seed-keyed counter) mod the integer weight
+    total, inverted by ``searchsorted`` on the integer CDF; edges are the
+    distinct keys u*|V|+v of ``m`` draws (so |E| is slightly below m).  All
+    arithmetic is integer, so the graph is bit-identical on CPU and GPU; on a
+    B200 it takes about a second instead of the numpy recipe's minutes.
+    Returns torch tensors (u_off, u_idx, v_off, v_idx) on ``device``.
+    """
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    cdf_u = torch.from_numpy(_capped_cdf(nu, gamma_u, cap_u, m)).to(dev)
+    cdf_v = torch.from_numpy(_capped_cdf(nv, gamma_v, cap_v, m)).to(dev)
+    tot_u, tot_v = int(cdf_u[-1]), int(cdf_v[-1])
+    ku, kv = _s64((seed * 0x632BE59BD9B4E019 + 1) % (1 << 64)), _s64((seed * 0x8CB92BA72F3D8DD7 + 2) % (1 << 64))
+    keys = torch.empty(m, dtype=torch.int64, device=dev)
+    mask63 = (1 << 63) - 1
+    for c0 in range(0, m, chunk):
+        c1 = min(m, c0 + chunk)
+        ctr = torch.arange(c0, c1, dtype=torch.int64, device=dev)
+        ru = (splitmix64(ctr ^ ku) & mask63) % tot_u
+        rv = (splitmix64(ctr ^ kv) & mask63) % tot_v
+        eu = torch.searchsorted(cdf_u, ru, right=True)
+        ev = torch.searchsorted(cdf_v, rv, right=True)
+        keys[c0:c1] = eu * nv + ev
+        del ctr, ru, rv, eu, ev
+    crng = np.random.default_rng(core_seed)
+    extra = []
+    for _ in range(n_cores):
+        for a, b, dens in PLANTED_CORES:
+            pu = crng.choice(nu, a, replace=False).astype(np.int64)
+            pv = crng.choice(nv, b, replace=False).astype(np.int64)
+            i, j = np.nonzero(crng.random((a, b)) < dens)
+            extra.append(pu[i] * nv + pv[j])
+    if extra:
+        keys = torch.cat([keys, torch.from_numpy(np.concatenate(extra)).to(dev)])
+    keys = torch.unique(keys, sorted=True)
+    return csr_from_sorted_keys_torch(nu, nv, keys)
+
+
+def csr_from_sorted_keys_torch(nu: int, nv: int, key):
+    """(u_off, u_idx, v_off, v_idx) torch tensors from strictly increasing keys."""
+    import torch
+
+    dev = key.device
+    su = key // nv
+    sv = key - su * nv
+    u_off = torch.zeros(nu + 1, dtype=torch.int64, device=dev)
+    u_off[1:] = torch.cumsum(torch.bincount(su, minlength=nu), 0)
+    u_idx = sv.to(torch.int32)
+    k2 = torch.sort(sv * nu + su).values  # V-major, u ascending inside each row
+    del sv
+    v_of = k2 // nu
+    v_off = torch.zeros(nv + 1, dtype=torch.int64, device=dev)
+    v_off[1:] = torch.cumsum(torch.bincount(v_of, minlength=nv), 0)
+    v_idx = (k2 - v_of * nu).to(torch.int32)
+    return u_off, u_idx, v_off, v_idx
+
+
+def graph_from_torch_csr(u_off, u_idx, v_off, v_idx) -> BipartiteGraph:
+    return BipartiteGraph.from_csr(u_off.cpu().numpy(), u_idx.cpu().numpy(),
+                                   v_off.cpu().numpy(), v_idx.cpu().numpy())
+
+
 CONFIGS = {
     # name: (builder, [(p, q), ...])
     "C1": (lambda: erdos_renyi(2000, 2000, 20000, 1), [(2, 2)]),
