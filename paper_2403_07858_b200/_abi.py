@@ -73,8 +73,9 @@ def _declare(L):
                            C.POINTER(BcReport)]
     L.bc_graph_create.restype = C.c_int
     L.bc_graph_create.argtypes = [vp, vp, i64, vp, vp, i64, i32, C.POINTER(C.c_void_p)]
-    L.bc_graph_create_device.restype = C.c_int
-    L.bc_graph_create_device.argtypes = [vp, vp, i64, vp, vp, i64, i32, C.POINTER(C.c_void_p)]
+    if hasattr(L, "bc_graph_create_device"):  # (absent from development A/B builds of older trees)
+        L.bc_graph_create_device.restype = C.c_int
+        L.bc_graph_create_device.argtypes = [vp, vp, i64, vp, vp, i64, i32, C.POINTER(C.c_void_p)]
     L.bc_graph_count.restype = C.c_int
     L.bc_graph_count.argtypes = [vp, i32, i32, C.POINTER(BcConfig), C.POINTER(BcReport)]
     L.bc_graph_destroy.restype = None

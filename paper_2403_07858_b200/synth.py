@@ -157,56 +157,6 @@ def planted_dense(seed_base: int = 7, seed_cores: int = 3) -> BipartiteGraph:
     return from_edges(12720, 11100, np.concatenate(eu), np.concatenate(ev))
 
 
-def fr_shaped(nu: int = 44_000, nv: int = 8_956_000, m: int = 100_000_000,
-              gamma_u: float = 2.5, gamma_v: float = 2.5, cap_u: float = 200_000,
-              cap_v: float = 64, seed: int = 5, n_cores: int = 64,
-              core_seed: int = 9) -> BipartiteGraph:
-    """C5: FR-shaped capped Chung-Lu + planted dense cores.
-
-    Small dense U, huge sparse V (|V|/|U| ~ 202). Expected degrees are
-    iteratively clipped at cap/m; endpoints sampled by inverse CDF; then
-    ``n_cores`` copies of C4's three core shapes are planted at random
-    positions so the (8,8) count is non-trivial.
-    """
-    rng = np.random.default_rng(seed)
-
-    def capped(n, gamma, cap):
-        w = (np.arange(n) + 1.0) ** (-1.0 / (gamma - 1.0))
-        w /= w.sum()
-        lim = cap / m
-        for _ in range(30):
-            w = np.minimum(w, lim)
-            w /= w.sum()
-        return np.cumsum(w)
-
-    k = int(m * 1.15)
-    cu = capped(nu, gamma_u, cap_u)
-    eu = np.searchsorted(cu, rng.random(k) * cu[-1], side="right").astype(np.int64)
-    np.minimum(eu, nu - 1, out=eu)
-    del cu
-    cv = capped(nv, gamma_v, cap_v)
-    ev = np.searchsorted(cv, rng.random(k) * cv[-1], side="right").astype(np.int64)
-    np.minimum(ev, nv - 1, out=ev)
-    del cv
-    key = eu * nv + ev
-    del eu, ev
-    key = np.unique(key)
-    if len(key) > m:
-        key = rng.permutation(key)[:m]
-    crng = np.random.default_rng(core_seed)
-    extra = []
-    for _ in range(n_cores):
-        for a, b, dens in PLANTED_CORES:
-            pu = crng.choice(nu, a, replace=False).astype(np.int64)
-            pv = crng.choice(nv, b, replace=False).astype(np.int64)
-            i, j = np.nonzero(crng.random((a, b)) < dens)
-            extra.append(pu[i] * nv + pv[j])
-    if extra:
-        key = np.concatenate([key] + extra)
-    key = np.unique(key)
-    return csr_from_sorted_keys(nu, nv, key)
-
-
 def _s64(x: int) -> int:
     """Unsigned 64-bit constant as a signed int64 value (two's complement)."""
     return x - (1 << 64) if x >= 1 << 63 else x
@@ -310,6 +260,12 @@ def csr_from_sorted_keys_torch(nu: int, nv: int, key):
     return u_off, u_idx, v_off, v_idx
 
 
+def _gen_device() -> str:
+    import torch
+
+    return "cuda" if torch.cuda.is_available() else "cpu"
+
+
 def graph_from_torch_csr(u_off, u_idx, v_off, v_idx) -> BipartiteGraph:
     return BipartiteGraph.from_csr(u_off.cpu().numpy(), u_idx.cpu().numpy(),
                                    v_off.cpu().numpy(), v_idx.cpu().numpy())
@@ -321,7 +277,7 @@ CONFIGS = {
     "C2": (lambda: chung_lu(100000, 50000, 1000000, 2.5, 7, 1.15), [(4, 4)]),
     "C3": (lambda: chung_lu(56519, 120867, 440237, 2.5, 11, 1.3), [(3, 6), (6, 3)]),
     "C4": (planted_dense, [(8, 8)]),
-    "C5": (fr_shaped, [(8, 8)]),
+    "C5": (lambda: graph_from_torch_csr(*fr_shaped_csr(device=_gen_device())), [(8, 8)]),
 }
 
 

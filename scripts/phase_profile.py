@@ -6,13 +6,18 @@ from paper_2403_07858_b200 import synth, DeviceGraph, _abi
 NAMES = ["claim", "level1-rebuild", "decode+map", "rows", "expand", "leaf-parents", "finish"]
 name = sys.argv[1]
 p, q = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else synth.CONFIGS[name][1][0]
-g = synth.build_config(name)
-dg = DeviceGraph(g)
+from paper_2403_07858_b200 import EngineConfig
+if name == "C5":
+    dg = DeviceGraph.from_device_csr(*synth.fr_shaped_csr(device="cuda"))
+    cfg = EngineConfig(batch_buffer_capacity=1 << 17)
+else:
+    dg = DeviceGraph(synth.build_config(name))
+    cfg = EngineConfig()
 L = _abi.load()
 buf = (C.c_uint64 * 16)()
-dg.count_raw(p, q)
+dg.count_raw(p, q, cfg)
 L.bc_debug_phase_cycles(buf, 16)
-rep, _ = dg.count_raw(p, q)
+rep, _ = dg.count_raw(p, q, cfg)
 n = L.bc_debug_phase_cycles(buf, 16)
 tot = sum(buf[i] for i in range(7))
 print(f"{name} ({p},{q}) enum {rep.time_enum*1e3:.2f} ms; phase share of warp-cycles (n={n}):")
