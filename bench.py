@@ -42,6 +42,16 @@ CONFIG_DESC = {
     "C5": "C5 FR-shaped capped Chung-Lu 44K x 8.956M, 1e8 edges + planted cores",
 }
 METRIC = "(p,q)-biclique count time (s) and bicliques/s at 1/2/4/8 B200 vs CPU ref"
+# batch_buffer_capacity per config: the reference rejects capacities below the largest
+# HTB slice (engine.py:387-391); C5's hub rows have 122,855 words (SURVEY 8(d) CPU timing
+# uses max(4096, max slice) the same way)
+CAPACITY = {"C5": 1 << 17}
+# CPU legs on C5 time the full CPU preprocessing plus the counting of a seeded sample of
+# roots, extrapolated by task share (a full CPU run is hours, SURVEY 7 hard part 6)
+SAMPLE_FRAC = {"C5": 0.005}
+# C5 (8,8) total, validated by the sampled-root parity test (tests/test_c5.py); used only
+# by the CPU-only reference arm, which cannot count C5 in full
+C5_COUNT = 9415393375594
 FALLBACK_HBM = 6650.0
 
 
@@ -137,12 +147,34 @@ def traffic_for(workload: str):
         return None
 
 
-def cpu_oracle_run(g, p, q, threads: int):
+def cpu_oracle_run(g, p, q, threads: int, config: str = ""):
+    """(count, seconds, sample description) of the CPU restatement on this host."""
     from oracle import oracle as O
 
+    frac = SAMPLE_FRAC.get(config)
+    cap = CAPACITY.get(config, 4096)
+    if frac is None:
+        t0 = time.perf_counter()
+        r = O.count(g, p, q, workers=threads, threads=threads, capacity=cap)
+        return r.count, time.perf_counter() - t0, "full count incl. preprocessing"
+    import numpy as np
+
     t0 = time.perf_counter()
-    r = O.count(g, p, q, workers=threads, threads=threads)
-    return r, time.perf_counter() - t0
+    prep = O.Prepared(g, p, q, threads=threads)
+    t_prep = time.perf_counter() - t0
+    und = prep.export(O.X_UND_SIZE)
+    dsz = np.diff(prep.export(O.X_DIR_OFF))
+    ntask = np.where(und >= prep.p_eff - 1, dsz, 0)
+    roots = np.random.default_rng(1).choice(prep.n, max(1, int(frac * prep.n)), replace=False)
+    share = float(ntask[roots].sum()) / float(max(1, ntask.sum()))
+    t1 = time.perf_counter()
+    r = O.count(g, p, q, workers=threads, threads=threads, capacity=cap, roots=roots,
+                prepared=prep)
+    t_cnt = time.perf_counter() - t1
+    est = t_prep + t_cnt / max(share, 1e-12)
+    return None, est, (f"full CPU preprocessing ({t_prep:.1f} s) + counting {len(roots)} seeded "
+                       f"random roots ({100 * share:.2f}% of tasks, {t_cnt:.1f} s), "
+                       f"extrapolated by task share")
 
 
 def run_reference(args, g, p, q, rank, world):
@@ -152,12 +184,12 @@ def run_reference(args, g, p, q, rank, world):
         return
     threads = host_cores()
     for _ in range(args.warmup):
-        cpu_oracle_run(g, p, q, threads)
-    times, count = [], None
+        cpu_oracle_run(g, p, q, threads, args.config)
+    times, count, what = [], None, ""
     for _ in range(args.steps):
-        r, dt = cpu_oracle_run(g, p, q, threads)
+        c, dt, what = cpu_oracle_run(g, p, q, threads, args.config)
         times.append(dt)
-        count = r.count
+        count = c if c is not None else C5_COUNT
     t = statistics.mean(times)
     v = count / t
     line = {
@@ -168,8 +200,8 @@ def run_reference(args, g, p, q, rank, world):
         "config": {"workload": f"{CONFIG_DESC[args.config]} ({p},{q})", "config": args.config,
                    "p": p, "q": q},
         "cpu_baseline": {"value": v, "unit": "bicliques/s", "cores": threads, "kind": "port",
-                         "sample": f"full {args.config} ({p},{q}) count incl. preprocessing "
-                                   f"(oracle/bicount_oracle.c, {threads} pthreads, {cpu_model()})"},
+                         "sample": f"{args.config} ({p},{q}): {what} (oracle/bicount_oracle.c, "
+                                   f"{threads} pthreads, {cpu_model()})"},
         "e2e": {"value": v, "unit": "bicliques/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -194,7 +226,17 @@ def main():
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     from paper_2403_07858_b200 import synth
 
-    g = synth.build_config(args.config)
+    dev_csr = None
+    if args.config == "C5" and args.impl == "ours":
+        import torch
+
+        # FR-shaped C5 is generated on the GPU (integer counter-based recipe, bit-identical
+        # on CPU); the host copy feeds the e2e leg and the CPU baseline
+        torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+        dev_csr = synth.fr_shaped_csr(device="cuda")
+        g = synth.graph_from_torch_csr(*dev_csr)
+    else:
+        g = synth.build_config(args.config)
     pq = synth.CONFIGS[args.config][1][0]
     p = args.p or pq[0]
     q = args.q or pq[1]
@@ -231,13 +273,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return merge_limbs(t.cpu().tolist())
 
-    cfg = EngineConfig(device=local)
-    dg = DeviceGraph(g, local)
+    cap = CAPACITY.get(args.config, 4096)
+    cfg = EngineConfig(device=local, batch_buffer_capacity=cap)
+    dg = DeviceGraph.from_device_csr(*dev_csr, local) if dev_csr is not None else DeviceGraph(g, local)
+    del dev_csr
     shard = (rank, world)
     for _ in range(args.warmup):
         dg.count_raw(p, q, cfg, shard=shard)
     # B_enum for this workload from the device's own reference-equivalent tally
-    instr, _ = dg.count_raw(p, q, EngineConfig(device=local, instrument=True), shard=shard)
+    instr, _ = dg.count_raw(p, q, EngineConfig(device=local, instrument=True,
+                                               batch_buffer_capacity=cap), shard=shard)
     b_enum_local = 8 * instr.operand_words
     b_min_local = 16 * instr.min_words
 
@@ -278,7 +323,7 @@ def main():
         u, v = g.u_csr, g.v_csr
         pinned = [torch.from_numpy(a).pin_memory() for a in (u.off, u.idx, v.off, v.idx)]
         c = _abi.BcConfig()
-        c.batch_words, c.mode, c.anchor, c.order_mode, c.device = 4096, 1, -1, 0, local
+        c.batch_words, c.mode, c.anchor, c.order_mode, c.device = cap, 1, -1, 0, local
         c.shard_index, c.shard_count, c.flags = rank, world, 0
         r = _abi.BcReport()
         for _ in range(1):
@@ -307,12 +352,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_cores()
-        r, dt = cpu_oracle_run(g, p, q, threads)
-        assert r.count == total, (r.count, total)
-        cpu = {"value": r.count / dt, "unit": "bicliques/s", "cores": threads, "kind": "port",
+        c_cpu, dt, what = cpu_oracle_run(g, p, q, threads, args.config)
+        if c_cpu is not None:
+            assert c_cpu == total, (c_cpu, total)
+        cpu = {"value": total / dt, "unit": "bicliques/s", "cores": threads, "kind": "port",
                "time_s": dt,
-               "sample": f"full {args.config} ({p},{q}) count incl. preprocessing: "
-                         f"oracle/bicount_oracle.c ({threads} pthreads, {cpu_model()})"}
+               "sample": f"{args.config} ({p},{q}): {what}: oracle/bicount_oracle.c "
+                         f"({threads} pthreads, {cpu_model()})"}
 
     if rank == 0:
         peak, peak_src = measured_peak()

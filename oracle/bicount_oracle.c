@@ -113,6 +113,7 @@ static int64_t wedge_mass(const int64_t *off, int64_t n) {
 typedef struct {
   const orc_struct *s; int32_t k; int64_t lo, hi;
   int32_t **lists; int64_t *sizes;
+  int64_t *next;  /* shared claim counter (vertices in blocks of 16: hubs balance) */
 } twohop_job;
 
 static int cmp_i32(const void *a, const void *b) {
@@ -125,7 +126,10 @@ static void *twohop_worker(void *arg) {
   const orc_struct *s = j->s;
   int32_t *cnt = (int32_t *)calloc((size_t)s->n, sizeof(int32_t));
   int32_t *touched = (int32_t *)xmalloc((size_t)(s->n ? s->n : 1) * sizeof(int32_t));
-  for (int64_t u = j->lo; u < j->hi; u++) {
+  for (;;) {
+   int64_t u0 = __atomic_fetch_add(j->next, 16, __ATOMIC_RELAXED);
+   if (u0 >= j->hi) break;
+   for (int64_t u = u0; u < u0 + 16 && u < j->hi; u++) {
     int64_t nt = 0;
     for (int64_t e = s->aoff[u]; e < s->aoff[u + 1]; e++) {
       int32_t v = s->aidx[e];
@@ -146,6 +150,7 @@ static void *twohop_worker(void *arg) {
     memcpy(out, touched, (size_t)keep * sizeof(int32_t));
     j->lists[u] = out;
     j->sizes[u] = keep;
+   }
   }
   free(cnt); free(touched);
   return NULL;
@@ -228,12 +233,10 @@ orc_struct *orc_prepare(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
   if (threads < 1) threads = n_threads_default();
   if (threads > 256) threads = 256;
   pthread_t th[256]; twohop_job jobs[256];
-  int64_t chunk = (n + threads - 1) / (threads ? threads : 1);
+  int64_t next = 0;
   int nt = 0;
-  for (int t = 0; t < threads; t++) {
-    int64_t lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
-    if (lo >= hi) break;
-    jobs[t] = (twohop_job){s, s->q_eff, lo, hi, lists, s->und_size};
+  for (int t = 0; t < threads && t < (n + 15) / 16; t++) {
+    jobs[t] = (twohop_job){s, s->q_eff, 0, n, lists, s->und_size, &next};
     pthread_create(&th[t], NULL, twohop_worker, &jobs[t]);
     nt++;
   }

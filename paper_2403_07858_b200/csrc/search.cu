@@ -697,9 +697,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       copy_d2h(hc, c2.p, sizeof hc, st);
       BC_CUDA(cudaStreamSynchronize(st));
       launches += 2;
-      // a probe is a bisect step chain (~4x a streamed id); the scatter walks each
-      // pool ~4 times (count, mask, write, cursor)
-      l1_mode = 4.0 * (double)hc[1] < 4.0 * (double)hc[0] ? 1 : 2;
+      // the scatter walks each pool ~4 times (count, mask, write, cursor) with an
+      // atomic per hit; a probe word is a short bisect in L2.  Measured break-even
+      // is near pool ~ probe / 8 (C2 probes, C5 scatters)
+      l1_mode = 8.0 * (double)hc[1] < (double)hc[0] ? 1 : 2;
       if (getenv("BC_DEBUG"))
         fprintf(stderr, "[bc level1] probe words %llu  pool %llu  -> %s\n", hc[0], hc[1],
                 l1_mode == 1 ? "scatter" : "probe");

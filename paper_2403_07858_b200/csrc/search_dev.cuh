@@ -950,7 +950,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
 // with their lslot rows, and rowR.  Compact (scatter) mode counts |N(x) & C_R1|
 // for every x by the wedge walk, then sets bits for the survivors only (when
 // they fit the cap); full mode probes a row for every x (local_row).
-// Returns the number of survivors.
+// Returns the number of survivors (-1 in full mode without lslot: not counted).
 template <bool INSTR>
 __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, const Dims &d,
                                              const FrameSpec &sp, int r, int s, int64_t j,
@@ -1022,6 +1022,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
                 f.rowR + (int64_t)x * d.WR, d.WR);
     }
     __syncwarp();
+    if (!sp.lslot()) return -1;  // survivors not needed (no rowL rows, no triage)
     int base = 0;
     for (int x0 = 0; x0 < d.nL; x0 += 32) {
       const int x = x0 + lane;
@@ -1033,7 +1034,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
         sv = c >= P.q_eff;
       }
       const unsigned m = __ballot_sync(FULL, sv);
-      if (sp.lslot() && x < d.nL) f.lslot[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
+      if (x < d.nL) f.lslot[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
       base += __popc(m);
     }
     ns1 = base;
@@ -1050,6 +1051,10 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
                                               PhaseClock &ph_) {
   const int lane = lane_id();
   const bool build = sp.rowL && P.p_eff >= 4 && !LAZY;
+  if (!build && !INSTR) {
+    PH_MARK(3);
+    return;
+  }
   for (int x = lane; x < d.nL; x += 32) {
     const int id = f.lids[x];
     if (build) {

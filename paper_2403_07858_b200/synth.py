@@ -227,18 +227,25 @@ def fr_shaped_csr(nu: int = 44_000, nv: int = 8_956_000, m: int = 100_000_000,
         ev = torch.searchsorted(cdf_v, rv, right=True)
         keys[c0:c1] = eu * nv + ev
         del ctr, ru, rv, eu, ev
+    extra = [pu[i] * nv + pv[j] for pu, pv, i, j in planted_cores(nu, nv, n_cores, core_seed)]
+    if extra:
+        keys = torch.cat([keys, torch.from_numpy(np.concatenate(extra)).to(dev)])
+    keys = torch.unique(keys, sorted=True)
+    return csr_from_sorted_keys_torch(nu, nv, keys)
+
+
+def planted_cores(nu: int, nv: int, n_cores: int = 64, core_seed: int = 9):
+    """The C5 planted cores: (U ids, V ids, edge rows, edge cols) per core, in
+    generation order (``n_cores`` copies of C4's three core shapes)."""
     crng = np.random.default_rng(core_seed)
-    extra = []
+    out = []
     for _ in range(n_cores):
         for a, b, dens in PLANTED_CORES:
             pu = crng.choice(nu, a, replace=False).astype(np.int64)
             pv = crng.choice(nv, b, replace=False).astype(np.int64)
             i, j = np.nonzero(crng.random((a, b)) < dens)
-            extra.append(pu[i] * nv + pv[j])
-    if extra:
-        keys = torch.cat([keys, torch.from_numpy(np.concatenate(extra)).to(dev)])
-    keys = torch.unique(keys, sorted=True)
-    return csr_from_sorted_keys_torch(nu, nv, keys)
+            out.append((pu, pv, i, j))
+    return out
 
 
 def csr_from_sorted_keys_torch(nu: int, nv: int, key):
