@@ -190,6 +190,28 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
   }
 }
 
+// upper bound on the 2-hop output: per anchor u, the kept ids (multiplicity >= k)
+// number at most min(n - 1, pool(u) / k), pool(u) = sum_{v in N(u)} deg(v)
+__global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
+                             const int64_t *__restrict__ boff, int64_t n, uint32_t k,
+                             unsigned long long *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long tot = 0;
+  for (int64_t u = gw; u < n; u += nw) {
+    unsigned long long pool = 0;
+    for (int64_t e = aoff[u] + lane; e < aoff[u + 1]; e += 32) {
+      const int v = aidx[e];
+      pool += (unsigned long long)(boff[v + 1] - boff[v]);
+    }
+    pool = warp_sum(pool);
+    const unsigned long long b = pool / k;
+    tot += b < (unsigned long long)(n - 1) ? b : (unsigned long long)(n - 1);
+  }
+  if (lane == 0 && tot) atomicAdd(out, tot);
+}
+
 // vertices by descending degree (LPT order for the 2-hop CTAs)
 __global__ void degree_keys(const int64_t *off, int64_t n, unsigned long long *keys) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -530,13 +552,18 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     L += 3;
     seg_start.alloc((size_t)n * ntiles, st);
     seg_len.alloc((size_t)n * ntiles, st);
-    // output capacity: the pool bound, capped; retried exactly on overflow
-    const int64_t pool_cap = std::min<int64_t>((int64_t)n * (n - 1), int64_t(1) << 31);
-    int64_t cap = std::min<int64_t>(pool_cap, std::max<int64_t>(int64_t(1) << 24, 64 * n));
+    // output capacity: the pool bound (exact upper bound; int32 offsets cap it at 2^31,
+    // an overflow past that is retried at the exact size)
     DBuf<int> ctrs;  // [0] next vertex, [1] overflow
     DBuf<unsigned long long> used;
     ctrs.alloc(2, st);
     used.alloc(1, st);
+    used.zero();
+    twohop_bound<<<warp_blocks(n, sms), 256, 0, st>>>(s.aoff, s.aidx, s.boff, n, k, used.p);
+    BC_CHECK_LAUNCH();
+    L++;
+    int64_t cap = std::min<int64_t>((int64_t)d2h_scalar(used.p, st), int64_t(1) << 31);
+    cap = std::max<int64_t>(cap, 1);
     for (int attempt = 0; attempt < 2; attempt++) {
       und_ids.alloc(cap, st);
       ctrs.zero();

@@ -489,15 +489,29 @@ __global__ void iota32(int32_t *a, int64_t n) {
 }
 
 // frame / sub-task arena sizes for queue[q0, q1)
-__global__ void split_sizes(const Info *info, const int32_t *queue, int64_t q0, int64_t q1,
-                            bool instr, int split_level, int64_t *ro, int64_t *sub) {
+// frame and sub-task arena words of queue[q0, q1): rows and split-level nodes are
+// bounded by the level-1 survivor count when triage measured it (caps), else |C_L1|
+__global__ void split_sizes(const Info *info, const int32_t *queue, const int32_t *caps,
+                            int64_t q0, int64_t q1, bool instr, int split_level, int64_t *ro,
+                            int64_t *sub) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= q1 - q0) return;
   const Info in = info[queue[q0 + i]];
-  ro[i] = ro_words(in.cr, in.cl, in.wr, in.wl, FrameSpec{true, true, instr, 0});
-  const int64_t WR = (in.cr + 31) / 32, WL = (in.cl + 31) / 32;
-  const int64_t nodes = split_level == 2 ? in.cl : (int64_t)in.cl * (in.cl - 1) / 2;
+  const int cap = caps ? caps[q0 + i] : 0;
+  const FrameSpec sp{true, true, instr, cap};
+  ro[i] = ro_words(in.cr, in.cl, in.wr, in.wl, sp);
+  const int64_t WR = (in.cr + 31) / 32, WL = (in.cl + 31) / 32, ns = sp.rows(in.cl);
+  const int64_t nodes = split_level == 2 ? ns : ns * (ns - 1) / 2;
   sub[i] = nodes * (4 + WR + WL);
+}
+
+__global__ void gather2(const int32_t *perm, int64_t n, const int32_t *a, const int32_t *b,
+                        int32_t *oa, int32_t *ob) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    oa[i] = a[perm[i]];
+    ob[i] = b[perm[i]];
+  }
 }
 
 // sub-task LPT key: candidates left below the node, |L| * |R| (saturating)
@@ -957,8 +971,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           // at most T level-1 R-survivors (whose frame fits the scratch) finishes in
           // place, the rest are deferred, heaviest first, to the split path below.
           int64_t n_heavy = n_alive;
-          const int32_t *hq_p = queue.p;
-          DBuf<int32_t> heavy, hq;
+          const int32_t *hq_p = queue.p, *hcap_p = nullptr;
+          DBuf<int32_t> heavy, heavy_ns1, hq, hcap;
           // triage only when splitting everything would not fit one frame arena
           // (millions of mostly light tasks, e.g. C5); C3/C4-sized queues split all
           int T = env_int("BC_TRIAGE", 48);
@@ -968,7 +982,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             sub_all.alloc(n_alive, st);
             sum.alloc(1, st);
             split_sizes<<<(unsigned)((n_alive + 255) / 256), 256, 0, st>>>(
-                info.p, queue.p, 0, n_alive, instr, s.p_eff <= 6 ? 2 : 3, ro_all.p, sub_all.p);
+                info.p, queue.p, nullptr, 0, n_alive, instr, s.p_eff <= 6 ? 2 : 3, ro_all.p,
+                sub_all.p);
             size_t tmp = 0;
             BC_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, ro_all.p, sum.p, n_alive, st));
             DBuf<char> tb;
@@ -986,6 +1001,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             const EnumVariant ev{instr, false, false, true};
             const int64_t blocks = (int64_t)sms * eblocks(ev, smem);
             heavy.alloc(n_alive, st);
+            heavy_ns1.alloc(n_alive, st);
             EnumArgs B = A;
             B.q0 = 0;
             B.q1 = n_alive;
@@ -993,6 +1009,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             B.triage = T;
             B.triage_work = env_int("BC_TRIAGE_WORK", 1 << 16);
             B.heavy = heavy.p;
+            B.heavy_ns1 = heavy_ns1.p;
             DBuf<uint32_t> gs;
             if (max_ro + max_scr > budget) {
               // per-warp frame scratch, capped at 4 GiB in total (larger frames defer)
@@ -1011,19 +1028,28 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             copy_d2h(&hn, ctr.p + CTR_HEAVY, sizeof hn, st);
             BC_CUDA(cudaStreamSynchronize(st));
             n_heavy = (int64_t)hn;
-            if (n_heavy > 0) {  // deferred tasks in LPT order again (deterministic)
+            if (n_heavy > 0) {  // deferred tasks in LPT order again, with their survivor caps
               DBuf<uint32_t> hk, hk2;
+              DBuf<int32_t> slot, perm;
               hk.alloc(n_heavy, st);
               hk2.alloc(n_heavy, st);
+              slot.alloc(n_heavy, st);
+              perm.alloc(n_heavy, st);
               hq.alloc(n_heavy, st);
+              hcap.alloc(n_heavy, st);
               gather_keys<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(heavy.p, n_heavy,
                                                                               cost.p, hk.p);
-              sort_pairs_desc(hk.p, hk2.p, heavy.p, hq.p, n_heavy, st);
-              launches += 2;
+              iota32<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(slot.p, n_heavy);
+              sort_pairs_desc(hk.p, hk2.p, slot.p, perm.p, n_heavy, st);
+              gather2<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(
+                  perm.p, n_heavy, heavy.p, heavy_ns1.p, hq.p, hcap.p);
+              launches += 4;
             }
             hq_p = hq.p;
+            hcap_p = hcap.p;
           }
           A.queue = hq_p;
+          A.caps = hcap_p;
           if (n_heavy > 0) {
           // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
             // writes every frame to the frame arena and pushes the split-level nodes,
@@ -1045,7 +1071,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               gs.alloc((size_t)blocks * wpb * A.gscratch_words, st);
               A.gscratch = gs.p;
             }
-            const int64_t arena_limit = int64_t(1) << 28;  // words per arena (1 GiB)
+            const int64_t arena_limit = int64_t(1) << 29;  // words per arena (2 GiB)
             DBuf<int64_t> ro, sub, foff, soff;
             ro.alloc(n_heavy + 1, st);
             sub.alloc(n_heavy + 1, st);
@@ -1054,7 +1080,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             ro.zero();
             sub.zero();
             split_sizes<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(
-                info.p, hq_p, 0, n_heavy, instr, split_level, ro.p, sub.p);
+                info.p, hq_p, hcap_p, 0, n_heavy, instr, split_level, ro.p, sub.p);
             scan_excl(ro.p, foff.p, n_heavy + 1, st);
             scan_excl(sub.p, soff.p, n_heavy + 1, st);
             std::vector<int64_t> hf(n_heavy + 1), hs(n_heavy + 1);

@@ -786,7 +786,7 @@ struct SplitSink {
   int level;                // emit nodes of this level instead of descending
   int64_t frame_off;        // this task's read-only frame in the frame arena
   int task_j;               // local task index
-  bool compact;             // frame layout (FrameSpec::compact)
+  int cap;                  // frame layout: FrameSpec::cap of the task
 };
 
 // Push node (level lv, sets R, L) as a sub-task; false if the arena is full.
@@ -811,7 +811,7 @@ __device__ __forceinline__ bool emit_node(const Params &P, const SplitSink &S, c
   uint32_t *rec = S.arena + off;
   if (lane == 0) {
     rec[0] = (uint32_t)S.task_j;
-    rec[1] = (uint32_t)lv | (S.compact ? 0x100u : 0u);
+    rec[1] = (uint32_t)lv | ((uint32_t)S.cap << 8);
     rec[2] = (uint32_t)(S.frame_off & 0xffffffffll);
     rec[3] = (uint32_t)(S.frame_off >> 32);
   }
@@ -1113,8 +1113,16 @@ struct EnumArgs {
   const unsigned long long *sub_order;  // sub_kernel: record offsets, LPT order
   int triage;                           // > 0: defer tasks with more level-1 R-survivors,
   long long triage_work;                //   more expansion work, or a frame over
-  int32_t *heavy;                       //   the scratch to heavy[] (the split path)
+  int32_t *heavy;                       //   the scratch to heavy[] (the split path),
+  int32_t *heavy_ns1;                   //   with their level-1 survivor counts (0: unknown)
+  const int32_t *caps;                  // SPLIT: survivor cap per queue entry (0: |C_L1|)
 };
+
+__device__ __forceinline__ void push_heavy(const Params &P, const EnumArgs &A, int j, int ns1) {
+  const unsigned long long k = atomicAdd(P.ctr + CTR_HEAVY, 1ull);
+  A.heavy[k] = j;
+  A.heavy_ns1[k] = ns1;
+}
 
 __device__ __forceinline__ void finish_task(const Params &P, Acc128 acc, int64_t t, bool atomic,
                                             Acc128 &total) {
@@ -1194,7 +1202,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
     const int2 tk = P.tasks[t];
     const Dims d = dims_of(A.info[j]);
     const FrameSpec sp{SPLIT || has_rowL(p_eff, P.map_words), COMPACT, INSTR,
-                       TRIAGE ? A.triage : 0};
+                       TRIAGE ? A.triage : (SPLIT && A.caps ? A.caps[qi] : 0)};
     const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, sp);
     const int64_t sc = scratch_words(d.nR, d.nL, p_eff, sp);
     uint32_t *ro_base, *sc_base;
@@ -1212,7 +1220,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
     }
     if (!sc_base || (sc_base == my_global && (SPLIT ? sc : ro + sc) > A.gscratch_words)) {
       if (TRIAGE) {  // frame too large for the scratch: the split path takes it
-        if (lane == 0) A.heavy[atomicAdd(P.ctr + CTR_HEAVY, 1ull)] = j;
+        if (lane == 0) push_heavy(P, A, j, 0);
         __syncwarp();
       } else if (lane == 0) {
         atomicExch(P.overflow, 2);  // cannot happen: sized from level-1 maxima
@@ -1224,7 +1232,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
     carve_scratch(f, sc_base, d, p_eff, sp);
     const int ns1 = build_frame_R<INSTR>(P, f, d, sp, tk.x, tk.y, j, map, ph_);
     if (TRIAGE && ns1 > A.triage) {  // too many survivor rows: split path
-      if (lane == 0) A.heavy[atomicAdd(P.ctr + CTR_HEAVY, 1ull)] = j;
+      if (lane == 0) push_heavy(P, A, j, ns1);
       clear_map(map, f, d);
       continue;
     }
@@ -1243,14 +1251,14 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
       SplitSink sink = A.sink;
       sink.frame_off = A.frame_off[qi - A.q0];
       sink.task_j = j;
-      sink.compact = COMPACT;
+      sink.cap = sp.cap;
       dfs<INSTR, false>(P, f, d, 1, map, lb, acc, tl, &sink, ph_);
     } else if (TRIAGE) {
       const Tally tl0 = tl;
       if (!dfs<INSTR, LAZY>(P, f, d, 1, map, lb, acc, tl, nullptr, ph_, A.triage_work)) {
         // over the work budget: discard the partial task, the split path takes it
         tl = tl0;
-        if (lane == 0) A.heavy[atomicAdd(P.ctr + CTR_HEAVY, 1ull)] = j;
+        if (lane == 0) push_heavy(P, A, j, ns1);
         clear_map(map, f, d);
         continue;
       }
@@ -1290,7 +1298,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
     const uint32_t *rec = A.sink.arena + A.sub_order[k];
     const int j = (int)rec[0];
     const int lv = (int)(rec[1] & 0xff);
-    const FrameSpec sp{true, COMPACT, INSTR, 0};
+    const FrameSpec sp{true, COMPACT, INSTR, (int)(rec[1] >> 8)};
     const int64_t foff = (int64_t)rec[2] | ((int64_t)rec[3] << 32);
     const int64_t t = P.shard + (int64_t)j * P.nshards;
     const Dims d = dims_of(A.info[j]);
