@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
           key = c > 0xfffffffeull ? 0xffffffffu : (uint32_t)(c ? c : 1);
           alive++;
           const FrameSpec sp{has_rowL(P.p_eff, P.map_words), true, INSTR, 0};  // upper bound
-          const unsigned long long ro = ro_words(cr, cl, wr, wl, sp);
+          const unsigned long long ro = ro_words_any(cr, cl, wr, wl, sp);
           const unsigned long long sc = scratch_words(cr, cl, P.p_eff, sp);
           maxro = ro > maxro ? ro : maxro;
           maxscr = sc > maxscr ? sc : maxscr;
@@ -492,13 +492,13 @@ __global__ void iota32(int32_t *a, int64_t n) {
 // frame and sub-task arena words of queue[q0, q1): rows and split-level nodes are
 // bounded by the level-1 survivor count when triage measured it (caps), else |C_L1|
 __global__ void split_sizes(const Info *info, const int32_t *queue, const int32_t *caps,
-                            int64_t q0, int64_t q1, bool instr, int split_level, int64_t *ro,
-                            int64_t *sub) {
+                            int64_t q0, int64_t q1, bool instr, bool compact, int split_level,
+                            int64_t *ro, int64_t *sub) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= q1 - q0) return;
   const Info in = info[queue[q0 + i]];
   const int cap = caps ? caps[q0 + i] : 0;
-  const FrameSpec sp{true, true, instr, cap};
+  const FrameSpec sp{true, compact, instr, cap};
   ro[i] = ro_words(in.cr, in.cl, in.wr, in.wl, sp);
   const int64_t WR = (in.cr + 31) / 32, WL = (in.cl + 31) / 32, ns = sp.rows(in.cl);
   const int64_t nodes = split_level == 2 ? ns : ns * (ns - 1) / 2;
@@ -975,15 +975,15 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           DBuf<int32_t> heavy, heavy_ns1, hq, hcap;
           // triage only when splitting everything would not fit one frame arena
           // (millions of mostly light tasks, e.g. C5); C3/C4-sized queues split all
-          int T = env_int("BC_TRIAGE", 48);
+          int T = env_int("BC_TRIAGE", 16);
           if (T > 0 && !env_int("BC_TRIAGE_FORCE", 0)) {
             DBuf<int64_t> ro_all, sub_all, sum;
             ro_all.alloc(n_alive, st);
             sub_all.alloc(n_alive, st);
             sum.alloc(1, st);
             split_sizes<<<(unsigned)((n_alive + 255) / 256), 256, 0, st>>>(
-                info.p, queue.p, nullptr, 0, n_alive, instr, s.p_eff <= 6 ? 2 : 3, ro_all.p,
-                sub_all.p);
+                info.p, queue.p, nullptr, 0, n_alive, instr, compact, s.p_eff <= 6 ? 2 : 3,
+                ro_all.p, sub_all.p);
             size_t tmp = 0;
             BC_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, ro_all.p, sum.p, n_alive, st));
             DBuf<char> tb;
@@ -996,7 +996,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             if (frames_total <= (int64_t(1) << 28)) T = 0;
           }
           if (T > 0) {
-            const int budget = env_int("BC_TRIAGE_BUDGET", 1536);
+            const int budget = env_int("BC_TRIAGE_BUDGET", 1024);
             const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
             const EnumVariant ev{instr, false, false, true};
             const int64_t blocks = (int64_t)sms * eblocks(ev, smem);
@@ -1080,7 +1080,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             ro.zero();
             sub.zero();
             split_sizes<<<(unsigned)((n_heavy + 255) / 256), 256, 0, st>>>(
-                info.p, hq_p, hcap_p, 0, n_heavy, instr, split_level, ro.p, sub.p);
+                info.p, hq_p, hcap_p, 0, n_heavy, instr, compact, split_level, ro.p, sub.p);
             scan_excl(ro.p, foff.p, n_heavy + 1, st);
             scan_excl(sub.p, soff.p, n_heavy + 1, st);
             std::vector<int64_t> hf(n_heavy + 1), hs(n_heavy + 1);

@@ -256,13 +256,23 @@ __host__ __device__ __forceinline__ int64_t ro_words(int nR, int nL, int wR, int
                                                      const FrameSpec &sp) {
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
   int64_t w = 3 * (int64_t)wR + 1 + 3 * (int64_t)wL + 1;  // C_R1 / C_L1 HTB words + prefixes
-  w += nL;                                                 // lids
+  if (!sp.compact) w += nL;                                // lids (compact: lid_of)
   if (sp.lslot()) w += nL;                                 // lslot
   if (sp.compact) w += nR;                                 // rids (C_R1 members)
   w += (sp.compact ? sp.rows(nL) : nL) * WR;               // rowR
   if (sp.rowL) w += sp.rows(nL) * WL;                      // rowL
   if (sp.instr) w += 2 * (int64_t)nL;                      // adj / dir2 slice words
   return (w + 3) & ~int64_t(3);
+}
+
+// frame words whichever row mode the launch uses (sizing before the choice)
+__host__ __device__ __forceinline__ int64_t ro_words_any(int nR, int nL, int wR, int wL,
+                                                         FrameSpec sp) {
+  sp.compact = false;
+  const int64_t a = ro_words(nR, nL, wR, wL, sp);
+  sp.compact = true;
+  const int64_t b = ro_words(nR, nL, wR, wL, sp);
+  return a > b ? a : b;
 }
 
 // DFS stack: nodes at levels 1 .. p_eff-3 are expanded warp-cooperatively
@@ -287,7 +297,7 @@ __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d,
   f.l_idx = p; p += d.wL;
   f.l_val = p; p += d.wL;
   f.l_pre = (int *)p; p += d.wL + 1;
-  f.lids = (int *)p; p += d.nL;
+  f.lids = (int *)p; if (!sp.compact) p += d.nL;
   f.lslot = (int *)p; if (sp.lslot()) p += d.nL;
   f.rids = (int *)p; if (sp.compact) p += d.nR;
   f.rowR = p; p += (sp.compact ? sp.rows(d.nL) : d.nL) * d.WR;
@@ -311,6 +321,19 @@ __device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims 
 
 __device__ __forceinline__ const uint32_t *rowL_of(const Frame &f, const Dims &d, int u) {
   return f.rowL + (int64_t)f.lslot[u] * d.WL;
+}
+
+// anchor id of C_L1 local index x: decoded list (full mode) or, in compact mode,
+// the word holding x (bisect on the prefix counts) and its bit of that rank
+__device__ __forceinline__ int lid_of(const Frame &f, const Dims &d, int x) {
+  if (!f.compact) return f.lids[x];
+  int lo = 0, hi = d.wL - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (f.l_pre[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return (int)f.l_idx[lo] * 32 + (int)__fns(f.l_val[lo], 0, x - f.l_pre[lo] + 1);
 }
 
 // rowR of candidate u, or null when u has no row (not a level-1 R-survivor)
@@ -640,7 +663,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
       int64_t start = 0;
       int len = 0;
       if (act) {
-        const int id = f.lids[u];
+        const int id = lid_of(f, d, u);
         start = P.g.doff[id];
         len = (int)(P.g.doff[id + 1] - start);
       }
@@ -919,24 +942,33 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
     }
     const int excl = incl - len;
     const int T = __shfl_sync(FULL, incl, 31);
-    for (int r0 = 0; r0 < T; r0 += 32) {
-      const int pos = r0 + lane;
-      int sl = 0;  // owning member: the last lane whose exclusive offset is <= pos
+    constexpr int U = 4;  // gathers in flight per lane
+    for (int r0 = 0; r0 < T; r0 += 32 * U) {
+      int xs[U], own[U];
 #pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int c = sl + step;
-        const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
-        if (c < 32 && e <= pos) sl = c;
+      for (int u = 0; u < U; u++) {
+        const int pos = r0 + 32 * u + lane;
+        int sl = 0;  // owning member: the last lane whose exclusive offset is <= pos
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int c = sl + step;
+          const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
+          if (c < 32 && e <= pos) sl = c;
+        }
+        const int64_t st = __shfl_sync(FULL, start, sl);
+        const int ex = __shfl_sync(FULL, excl, sl);
+        own[u] = sl;
+        xs[u] = pos < T ? __ldg(P.g.bidx + st + (pos - ex)) : -1;
       }
-      const int64_t st = __shfl_sync(FULL, start, sl);
-      const int ex = __shfl_sync(FULL, excl, sl);
-      if (pos < T) {
-        const int x = __ldg(P.g.bidx + st + (pos - ex));
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int x = xs[u];
+        if (x < 0) continue;
         const int k = map[x >> 5];
         if (k != 0xffff) {
           const uint32_t lv = f.l_val[k];
           const int xb = x & 31;
-          if ((lv >> xb) & 1u) fn(b0 + sl, f.l_pre[k] + __popc(lv & ((1u << xb) - 1u)));
+          if ((lv >> xb) & 1u) fn(b0 + own[u], f.l_pre[k] + __popc(lv & ((1u << xb) - 1u)));
         }
       }
     }
@@ -967,10 +999,11 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     const int base_id = (int)f.l_idx[k] * 32;
     int pos = f.l_pre[k];
     if (map) map[f.l_idx[k]] = (uint16_t)k;
-    while (v) {
-      f.lids[pos++] = base_id + __ffs(v) - 1;
-      v &= v - 1;
-    }
+    if (!sp.compact)
+      while (v) {
+        f.lids[pos++] = base_id + __ffs(v) - 1;
+        v &= v - 1;
+      }
   }
   if (sp.compact) {  // C_R1 members, ascending
     for (int k = lane; k < d.wR; k += 32) {
@@ -1056,7 +1089,8 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
     return;
   }
   for (int x = lane; x < d.nL; x += 32) {
-    const int id = f.lids[x];
+    if (sp.compact && !INSTR && f.lslot[x] < 0) continue;
+    const int id = lid_of(f, d, x);
     if (build) {
       const int slot = f.lslot[x];
       if (slot >= 0) {
