@@ -235,6 +235,8 @@ struct Frame {
   int *r_pre;
   uint32_t *l_idx, *l_val;
   int *l_pre;
+  uint32_t *r_last;  // bit i: local C_R1 index i is the last of its HTB word
+  uint32_t *l_last;  // same for C_L1
   int *lids, *lslot, *rids;
   uint32_t *rowR, *rowL;
   int *adjw, *dirw;
@@ -256,6 +258,7 @@ __host__ __device__ __forceinline__ int64_t ro_words(int nR, int nL, int wR, int
                                                      const FrameSpec &sp) {
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
   int64_t w = 3 * (int64_t)wR + 1 + 3 * (int64_t)wL + 1;  // C_R1 / C_L1 HTB words + prefixes
+  w += WR + WL;                                            // r_last, l_last
   if (!sp.compact) w += nL;                                // lids (compact: lid_of)
   if (sp.lslot()) w += nL;                                 // lslot
   if (sp.compact) w += nR;                                 // rids (C_R1 members)
@@ -297,6 +300,8 @@ __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d,
   f.l_idx = p; p += d.wL;
   f.l_val = p; p += d.wL;
   f.l_pre = (int *)p; p += d.wL + 1;
+  f.r_last = p; p += d.WR;
+  f.l_last = p; p += d.WL;
   f.lids = (int *)p; if (!sp.compact) p += d.nL;
   f.lslot = (int *)p; if (sp.lslot()) p += d.nL;
   f.rids = (int *)p; if (sp.compact) p += d.nR;
@@ -466,44 +471,42 @@ __device__ __forceinline__ void local_row_map(const uint16_t *map, const uint32_
   rw.finish();
 }
 
-// Number of original HTB words (ranges [pre[k], pre[k+1])) a local bitset touches.
-__device__ __forceinline__ int words_touched(const uint32_t *set, const int *pre, int nwords,
-                                             int W, bool single) {
+// Number of original HTB words a local bitset touches (the reference's word count
+// of the node's set, engine.py:306-313), warp-parallel over the W local words with
+// the field trick of lane_words below.  A field (one HTB word's local indices) has
+// at most 32 bits, so it spans at most two words and a word's carry-out depends on
+// that word alone: each lane forms its carry-out, the next lane takes it as carry-in.
+__device__ __forceinline__ int words_touched(const uint32_t *set, const uint32_t *last, int W) {
+  const int lane = lane_id();
   int c = 0;
-  if (single) {
-    for (int w = lane_id(); w < W; w += 32) c += __popc(set[w]);
-  } else {
-    for (int k = lane_id(); k < nwords; k += 32) {
-      const int a = pre[k], b = pre[k + 1];
-      const int w0 = a >> 5, w1 = (b - 1) >> 5;
-      unsigned long long x = set[w0];
-      if (w1 > w0) x |= (unsigned long long)set[w1] << 32;
-      x >>= (a & 31);
-      const int len = b - a;
-      const unsigned long long mask = len >= 64 ? ~0ull : ((1ull << len) - 1ull);
-      c += (x & mask) != 0;
-    }
+  unsigned long long cin_chunk = 0;
+  for (int w0 = 0; w0 < W; w0 += 32) {
+    const int w = w0 + lane;
+    const uint32_t x = w < W ? set[w] : 0u, L = w < W ? last[w] : FULL;
+    const unsigned long long base = (unsigned long long)(x & ~L) + (unsigned long long)(~L);
+    const unsigned long long cout = base >> 32;
+    unsigned long long cin = __shfl_up_sync(FULL, cout, 1);
+    if (lane == 0) cin = cin_chunk;
+    c += __popc(((uint32_t)(base + cin) | x) & L);
+    cin_chunk = __shfl_sync(FULL, cout, 31);
   }
   return __reduce_add_sync(FULL, c);
 }
 
-// Same count for R & ru, by one lane.
-__device__ __forceinline__ int lane_words(const uint32_t *R, const uint32_t *ru, const int *pre,
-                                          int nwords, int W, bool single) {
+// Same count for X = R & ru, by one lane, in O(W) words: the local indices of
+// one HTB word form a field ending at a `last` bit; (X & ~last) + ~last, added
+// across words with carry, sets a field's last bit iff its low bits are non-zero
+// and never carries out of a field, so the touched fields are
+// popc(((X & ~last) + ~last | X) & last).
+__device__ __forceinline__ int lane_words(const uint32_t *R, const uint32_t *ru,
+                                          const uint32_t *last, int W) {
   int c = 0;
-  if (single) {
-    for (int w = 0; w < W; w++) c += __popc(R[w] & ru[w]);
-    return c;
-  }
-  for (int k = 0; k < nwords; k++) {
-    const int a = pre[k], b = pre[k + 1];
-    const int w0 = a >> 5, w1 = (b - 1) >> 5;
-    unsigned long long x = R[w0] & ru[w0];
-    if (w1 > w0) x |= (unsigned long long)(R[w1] & ru[w1]) << 32;
-    x >>= (a & 31);
-    const int len = b - a;
-    const unsigned long long mask = len >= 64 ? ~0ull : ((1ull << len) - 1ull);
-    c += (x & mask) != 0;
+  unsigned long long carry = 0;
+  for (int w = 0; w < W; w++) {
+    const uint32_t x = R[w] & ru[w], L = last[w];
+    const unsigned long long sum = (unsigned long long)(x & ~L) + (unsigned long long)(~L) + carry;
+    carry = sum >> 32;
+    c += __popc(((uint32_t)sum | x) & L);
   }
   return c;
 }
@@ -654,7 +657,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     const int i = base + lane;
     const bool act = i < n;
     const int u = act ? list[i] : 0;
-    const int wr = act ? lane_words(R, rowR_of(f, d, u), f.r_pre, d.wR, WR, d.r_single) : 0;
+    const int wr = act ? lane_words(R, rowR_of(f, d, u), f.r_last, WR) : 0;
     lb.wr[lane] = wr;
     lb.ncand[lane] = 0;
     __syncwarp();
@@ -736,8 +739,8 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
   const bool leaf = level + 1 == P.p_eff - 1;
   const bool lp = level + 1 == P.p_eff - 2;  // children are leaf-parents
   const int ncand = compact_bits(Ls, WL, f.cand);
-  const int wr = level == 1 ? d.wR : words_touched(R, f.r_pre, d.wR, WR, d.r_single);
-  const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_pre, d.wL, WL, d.l_single));
+  const int wr = level == 1 ? d.wR : words_touched(R, f.r_last, WR);
+  const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_last, WL));
   if (lane == 0) tl.batches += node_batches(P, (unsigned)ncand, wr, wl, leaf);
   int ns = 0;
   const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
@@ -1083,6 +1086,23 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
                                               const FrameSpec &sp, const uint16_t *map,
                                               PhaseClock &ph_) {
   const int lane = lane_id();
+  // word-boundary masks of the local universes for the batch accounting below level 1
+  // (C_R: leaf-parents and deeper nodes; C_L: nodes at level >= 2, p_eff >= 5)
+  const bool need_l = P.p_eff >= 5;
+  for (int w = lane; w < d.WR; w += 32) f.r_last[w] = 0;
+  if (need_l)
+    for (int w = lane; w < d.WL; w += 32) f.l_last[w] = 0;
+  __syncwarp();
+  for (int k = lane; k < d.wR; k += 32) {
+    const int e = f.r_pre[k + 1] - 1;
+    atomicOr(f.r_last + (e >> 5), 1u << (e & 31));
+  }
+  if (need_l)
+    for (int k = lane; k < d.wL; k += 32) {
+      const int e = f.l_pre[k + 1] - 1;
+      atomicOr(f.l_last + (e >> 5), 1u << (e & 31));
+    }
+  __syncwarp();
   const bool build = sp.rowL && P.p_eff >= 4 && !LAZY;
   if (!build && !INSTR) {
     PH_MARK(3);
