@@ -55,7 +55,12 @@ void validate_config(const bc_config &c) {
   if (c.anchor < -1 || c.anchor > 1) throw Error(BC_EINVAL, "anchor must be one of ('auto', 'U', 'V')");
   if (c.shard_count < 1 || c.shard_index < 0 || c.shard_index >= c.shard_count)
     throw Error(BC_EINVAL, "invalid shard_index / shard_count");
-  if (c.order_mode != 0) throw Error(BC_EINVAL, "order_mode must be 0 (reference)");
+  if (c.order_mode < 0 || c.order_mode > 2)
+    throw Error(BC_EINVAL, "order_mode must be one of ('reference', 'fast', 'fast-reorder')");
+  if (c.order_mode != 0 && c.rank_override)
+    throw Error(BC_EINVAL, "a rank override needs order_mode 'reference'");
+  if (c.order_mode != 0 && c.roots)
+    throw Error(BC_EINVAL, "roots= needs order_mode 'reference'");
 }
 
 void fill_from_structs(const bc::DevStructs &s, bc_report &out) {
@@ -215,6 +220,12 @@ void bc_graph_destroy(bc_graph *h) {
   delete h;
 }
 
+// temporary work graph of the fast order modes, freed on every exit path
+struct WorkGraph {
+  bc::DevGraph g;
+  ~WorkGraph() { bc::free_graph(g); }
+};
+
 static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_report *out) {
   try {
     if (!h || !cfg || !out) throw bc::Error(BC_EINVAL, "null argument");
@@ -227,7 +238,24 @@ static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, b
     BC_CUDA(cudaEventCreate(&a));
     BC_CUDA(cudaEventCreate(&b));
     BC_CUDA(cudaEventRecord(a, h->g.stream));
-    bc::prepare(h->g, p, q, *cfg, s);
+    // "fast" order modes: anchor choice on the input graph (graph.py:252-269), then the
+    // (q_eff, p_eff)-core of the work graph (optionally degree-relabelled) with that
+    // anchor as U; the count is the same, the structures and counters are not
+    WorkGraph work;
+    const bc::DevGraph *gp = &h->g;
+    bc_config c2 = *cfg;
+    int layer = -1, pp = p, qq = q;
+    if (cfg->order_mode != 0) {
+      layer = cfg->anchor < 0 ? (h->g.wedge_v <= h->g.wedge_u ? 0 : 1) : cfg->anchor;
+      pp = layer == 0 ? p : q;
+      qq = layer == 0 ? q : p;
+      int64_t L = 0;
+      bc::fast_order(h->g, layer, pp, qq, cfg->order_mode == 2, work.g, L);
+      out->kernel_launches += L;
+      c2.anchor = 0;
+      gp = &work.g;
+    }
+    bc::prepare(*gp, pp, qq, c2, s);
     BC_CUDA(cudaEventRecord(b, h->g.stream));
     // _build_shared capacity check (engine.py:382-391)
     const int64_t max_words = s.max_adj_slice > s.max_dir_slice ? s.max_adj_slice : s.max_dir_slice;
@@ -237,7 +265,8 @@ static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, b
                                      std::to_string(max_words) +
                                      " words); raise --batch-words");
     fill_from_structs(s, *out);
-    bc::search(s, *cfg, *out);
+    if (layer >= 0) out->anchor = layer;
+    bc::search(s, c2, *out);
     float ms = 0;
     BC_CUDA(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
@@ -300,6 +329,8 @@ int bc_prepare(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_struc
   try {
     if (!h || !cfg) throw bc::Error(BC_EINVAL, "null argument");
     validate_config(*cfg);
+    if (cfg->order_mode != 0)
+      throw bc::Error(BC_EINVAL, "structure export needs order_mode 'reference'");
     BC_CUDA(cudaSetDevice(h->g.device));
     r->g = &h->g;
     bc::prepare(h->g, p, q, *cfg, r->s);

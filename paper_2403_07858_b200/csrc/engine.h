@@ -110,6 +110,12 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out);
 
 int num_sms(int device);
 
+// "fast" order mode (order.cu): the (q_eff, p_eff)-core of the work graph (anchor
+// `layer` becomes U), optionally relabelled by degree; frees with free_graph.
+void fast_order(const DevGraph &g, int layer, int p_eff, int q_eff, bool reorder, DevGraph &out,
+                int64_t &launches);
+void free_graph(DevGraph &g);
+
 // BC_PHASE_PROF builds: per-phase SM cycles of the last enumeration (reset on read).
 int64_t debug_phase_cycles(uint64_t *out, int n);
 

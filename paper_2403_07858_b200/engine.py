@@ -28,7 +28,7 @@ from .graph import BipartiteGraph, CsrView, as_csr
 
 MODES = ("dfs", "hybrid")
 ANCHOR_FLAGS = ("auto", "U", "V")
-ORDER_MODES = ("reference",)
+ORDER_MODES = ("reference", "fast", "fast-reorder")
 KERNEL_CHOICES = ("auto", "scatter", "probe")
 
 

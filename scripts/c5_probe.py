@@ -27,7 +27,7 @@ del uo, ui, vo, vi
 torch.cuda.empty_cache()
 for it in range(int(os.environ.get("REPS", "1"))):
     t = time.time()
-    rep, _ = dg.count_raw(p, q, EngineConfig(instrument=bool(os.environ.get("INSTR")), batch_buffer_capacity=1 << 17))
+    rep, _ = dg.count_raw(p, q, EngineConfig(instrument=bool(os.environ.get("INSTR")), batch_buffer_capacity=1 << 17, order_mode=os.environ.get("ORDER", "reference")))
     d = rep.as_dict()
     print(f"({p},{q}) wall {time.time() - t:.3f} s count {d['count']} prep {rep.time_prep:.3f} "
           f"l1 {rep.time_level1:.3f} enum {rep.time_enum:.3f} tasks {rep.tasks_emitted} "

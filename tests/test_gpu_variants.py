@@ -66,3 +66,46 @@ def test_scatter_shards_and_task_counts():
         total += int(r.count_lo) | (int(r.count_hi) << 64)
     assert total == want.count
     dg.close()
+
+
+@pytest.mark.parametrize("order", ["fast", "fast-reorder"])
+def test_fast_order_counts(golden, order):
+    """(q,p)-core pruning (+ degree relabel): same exact counts as the reference order
+    on random graphs (all anchors, both modes), corpus300 and the C1-C4 configs."""
+    rng = np.random.default_rng(5)
+    for i in range(40):
+        nu, nv = int(rng.integers(10, 140)), int(rng.integers(10, 140))
+        g = synth.random_bipartite(nu, nv, float(rng.uniform(0.05, 0.45)), int(rng.integers(1 << 30)))
+        p, q = int(rng.integers(1, 9)), int(rng.integers(1, 8))
+        anchor = ["auto", "U", "V"][i % 3]
+        want = O.count(g, p, q, anchor=anchor).count
+        for rows in ("probe", "scatter"):
+            rep = count_bicliques(g, p, q, EngineConfig(anchor=anchor, order_mode=order, rows=rows,
+                                                        mode=["hybrid", "dfs"][i % 2]))
+            assert rep.count == want, (i, p, q, anchor, order, rows)
+    corpus = synth.corpus300()[:60]
+    pq = golden["corpus300"]["pq"]
+    for g, row in zip(corpus, golden["corpus300"]["counts"]):
+        dg = DeviceGraph(g)
+        for (p, q), want in zip(pq, row):
+            r, _ = dg.count_raw(p, q, EngineConfig(order_mode=order))
+            assert str(int(r.count_lo) | (int(r.count_hi) << 64)) == want, (p, q)
+        dg.close()
+    for name, (p, q) in [("C1", (2, 2)), ("C3", (3, 6)), ("C3", (6, 3)), ("C4", (8, 8))]:
+        g = synth.build_config(name)
+        want = golden["configs"][name][f"({p},{q})"]["hybrid"]["count"]
+        dg = DeviceGraph(g)
+        r, _ = dg.count_raw(p, q, EngineConfig(order_mode=order))
+        assert str(int(r.count_lo) | (int(r.count_hi) << 64)) == want, (name, order)
+        total = 0
+        for k in range(3):
+            rr, _ = dg.count_raw(p, q, EngineConfig(order_mode=order), shard=(k, 3))
+            total += int(rr.count_lo) | (int(rr.count_hi) << 64)
+        assert str(total) == want
+        dg.close()
+
+
+def test_fast_order_rejects_reference_only_inputs():
+    g = synth.random_bipartite(40, 40, 0.3, 3)
+    with pytest.raises(ValueError):
+        count_bicliques(g, 3, 3, EngineConfig(order_mode="fast"), roots=[0, 1])
