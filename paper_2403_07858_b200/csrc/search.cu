@@ -1130,12 +1130,17 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               A.sink.index = index.p;
               A.sink.index_cap = cap;
               A.sink.level = split_level;
+              dt.mark("split chunk setup");
               elaunch(ev, (unsigned)blocks, smem, P, A);
               unsigned long long hn = 0;
               copy_d2h(&hn, ctr.p + CTR_SUB_N, sizeof hn, st);
               BC_CUDA(cudaStreamSynchronize(st));
               const int64_t n_sub = std::min<int64_t>((int64_t)hn, cap);
               launches += 1;
+              if (dt.on)
+                fprintf(stderr, "[bc search] split chunk [%lld, %lld): frames %lld words, %lld sub-tasks\n",
+                        (long long)q0, (long long)q1, (long long)fw, (long long)n_sub);
+              dt.mark("split enum");
               if (n_sub > 0) {
                 DBuf<uint32_t> k0, k1;
                 DBuf<unsigned long long> v1;
@@ -1150,6 +1155,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
                 A.sub_order = v1.p;
                 if (compact) sub_launch_c1(instr, (unsigned)sblocks, ssmem, st, P, A, n_sub);
                 else sub_launch_c0(instr, (unsigned)sblocks, ssmem, st, P, A, n_sub);
+                dt.mark("split sub");
                 launches += 3;
               }
               n_sub_total += n_sub;

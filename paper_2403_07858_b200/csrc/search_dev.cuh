@@ -549,52 +549,22 @@ __device__ __forceinline__ unsigned node_batches(const Params &P, unsigned ncand
 }
 
 // Per-warp shared-memory staging of (leaf-parent slot, leaf) pairs.
-constexpr int LEAF_BUF = 256;
 struct LeafBuf {
-  uint32_t *pairs;  // [LEAF_BUF]: slot << 27 | local leaf index
-  int *wr;          // [32]: C_R word count of each slot's leaf-parent
-  int *ncand;       // [32]: leaves of each slot's leaf-parent (batch accounting)
+  int *wr;     // [32]: C_R word count of each slot's leaf-parent
+  int *ncand;  // [32]: leaves of each slot's leaf-parent (batch accounting)
 };
+constexpr int LEAF_WORDS = 64;  // per-warp leaf-parent bookkeeping in shared memory
 
-// Evaluate buffered leaves: add C(|R & rowR[u] & rowR[w]|, q) (engine.py:342-347).
+// Evaluate one round of leaves (engine.py:342-347): lane i offers the present bits m
+// of an HTB-style word (v, pre) for leaf-parent `slot`; all offered leaves, as one
+// flattened list, are spread over the 32 lanes (owner lane by a shuffle bisection
+// over the exclusive popcount prefix, leaf = that lane's k-th set bit), and each
+// adds C(|R & rowR[u] & rowR[w]|, q).
 template <bool INSTR>
-__device__ __forceinline__ void flush_leaves(const Params &P, const Frame &f, const Dims &d,
-                                             const uint32_t *R, const int *slot_u,
-                                             const LeafBuf &lb, int fill, Acc128 &acc,
-                                             Tally &tl) {
-  __syncwarp();
-  const int WR = d.WR, q = P.q_eff;
-  for (int p0 = 0; p0 < fill; p0 += 32) {
-    const int i = p0 + lane_id();
-    if (i < fill) {
-      const uint32_t pr = lb.pairs[i];
-      const int slot = pr >> 27, w = pr & 0x7ffffff;
-      const int u = slot_u[slot];
-      const uint32_t *ru = rowR_of(f, d, u), *rw = rowR_of(f, d, w);
-      int c = 0;
-      if (rw)
-        for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
-      if (INSTR) {
-        const int wr = lb.wr[slot];
-        tl.inter++;
-        tl.opw += wr + f.adjw[w];
-        tl.minw += wr < f.adjw[w] ? wr : f.adjw[w];
-      }
-      if (c >= q) add_comb(P, acc, c);
-    }
-  }
-  __syncwarp();
-}
-
-// Stage the leaves of one round: lane holds HTB-style word (v, pre) with
-// present bits m for leaf-parent `slot`; leaves are compacted into the pair
-// buffer (flushed 32 at a time when full).
-template <bool INSTR>
-__device__ __forceinline__ void stage_leaves(const Params &P, const Frame &f, const Dims &d,
-                                             const uint32_t *R, const int *slot_u,
-                                             const LeafBuf &lb, int &fill, int slot, uint32_t v,
-                                             int pre, uint32_t m, int wr, Acc128 &acc,
-                                             Tally &tl) {
+__device__ __forceinline__ void eval_leaves(const Params &P, const Frame &f, const Dims &d,
+                                            const uint32_t *R, const int *slot_u, int slot,
+                                            uint32_t v, int pre, uint32_t m, int wr, Acc128 &acc,
+                                            Tally &tl) {
   const int lane = lane_id();
   const int cnt = __popc(m);
   int incl = cnt;
@@ -603,38 +573,37 @@ __device__ __forceinline__ void stage_leaves(const Params &P, const Frame &f, co
     const int t = __shfl_up_sync(FULL, incl, o);
     if (lane >= o) incl += t;
   }
+  const int excl = incl - cnt;
   const int total = __shfl_sync(FULL, incl, 31);
-  if (fill + total > LEAF_BUF) {
-    flush_leaves<INSTR>(P, f, d, R, slot_u, lb, fill, acc, tl);
-    fill = 0;
-  }
-  if (total > LEAF_BUF) {  // a round too wide to stage: evaluate in place
-    const int WR = d.WR;
-    const uint32_t *ru = m ? rowR_of(f, d, slot_u[slot]) : nullptr;  // idle lanes: no slot
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int w = pre + __popc(v & ((1u << b) - 1u));
-      const uint32_t *rw = rowR_of(f, d, w);
+  const int WR = d.WR;
+  for (int r0 = 0; r0 < total; r0 += 32) {
+    const int k = r0 + lane;
+    int o = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int c = o + step;
+      const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
+      if (c < 32 && e <= k) o = c;
+    }
+    const int so = __shfl_sync(FULL, slot, o);
+    const uint32_t vo = __shfl_sync(FULL, v, o), mo = __shfl_sync(FULL, m, o);
+    const int po = __shfl_sync(FULL, pre, o), eo = __shfl_sync(FULL, excl, o);
+    const int wro = INSTR ? __shfl_sync(FULL, wr, o) : 0;
+    if (k < total) {
+      const int b = (int)__fns(mo, 0, k - eo + 1);
+      const int w = po + __popc(vo & ((1u << b) - 1u));
+      const uint32_t *ru = rowR_of(f, d, slot_u[so]), *rw = rowR_of(f, d, w);
       int c = 0;
       if (rw)
         for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
       if (INSTR) {
         tl.inter++;
-        tl.opw += wr + f.adjw[w];
-        tl.minw += wr < f.adjw[w] ? wr : f.adjw[w];
+        tl.opw += wro + f.adjw[w];
+        tl.minw += wro < f.adjw[w] ? wro : f.adjw[w];
       }
       if (c >= P.q_eff) add_comb(P, acc, c);
     }
-    return;
   }
-  int o = fill + incl - cnt;
-  while (m) {
-    const int b = __ffs(m) - 1;
-    m &= m - 1;
-    lb.pairs[o++] = ((uint32_t)slot << 27) | (uint32_t)(pre + __popc(v & ((1u << b) - 1u)));
-  }
-  fill += total;
 }
 
 // Leaf-parent nodes, 32 at a time (one slot per lane): node u (a survivor
@@ -642,8 +611,8 @@ __device__ __forceinline__ void stage_leaves(const Params &P, const Frame &f, co
 // with LAZY (p_eff = 4, level 1), L' = dir2(u) & C_L1 read through the slot
 // map -- and its children are leaves (engine.py:342-347).  The L' words of
 // the 32 leaf-parents are walked as one flattened stream (LAZY: every lane
-// loads a different dir2 word each round, so the gathers overlap), and the
-// leaves are compacted and evaluated 32 at a time.
+// loads a different dir2 word each round, so the gathers overlap), and each
+// round's leaves are spread over the lanes (eval_leaves).
 template <bool INSTR, bool LAZY>
 __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, const Dims &d,
                                              int level, const int *list, int n,
@@ -661,7 +630,6 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     lb.wr[lane] = wr;
     lb.ncand[lane] = 0;
     __syncwarp();
-    int fill = 0;
     if (LAZY) {
       int64_t start = 0;
       int len = 0;
@@ -703,7 +671,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
             if (m) atomicAdd(&lb.ncand[sl], __popc(m));
           }
         }
-        stage_leaves<INSTR>(P, f, d, R, list + base, lb, fill, sl, v, pre, m, lb.wr[sl], acc, tl);
+        eval_leaves<INSTR>(P, f, d, R, list + base, sl, v, pre, m, lb.wr[sl], acc, tl);
       }
     } else {
       int ncand = 0;
@@ -712,12 +680,10 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
         uint32_t m = 0;
         if (act && x < WL) m = Ls[x] & rl[x];
         ncand += __popc(m);
-        stage_leaves<INSTR>(P, f, d, R, list + base, lb, fill, lane, 0xffffffffu, x * 32, m, wr,
-                            acc, tl);
+        eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, acc, tl);
       }
       lb.ncand[lane] = ncand;
     }
-    flush_leaves<INSTR>(P, f, d, R, list + base, lb, fill, acc, tl);
     if (act) tl.batches += node_batches(P, (unsigned)lb.ncand[lane], wr, 0, true);
     __syncwarp();
   }
@@ -1219,7 +1185,6 @@ constexpr int ENUM_THREADS = 256;
 #ifndef ENUM_MIN_BLOCKS
 #define ENUM_MIN_BLOCKS 3
 #endif
-constexpr int LEAF_WORDS = LEAF_BUF + 64;  // per-warp leaf staging in shared memory
 
 // Whole tasks (SPLIT = false) or the top levels of every task with its frame
 // written to the global frame arena and split-level nodes pushed as sub-tasks
@@ -1233,7 +1198,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
   const int map_w = (P.map_words + 1) / 2;  // u16 entries packed in words
   uint32_t *my = smem + (int64_t)wib * (map_w + LEAF_WORDS + A.budget_words);
   uint16_t *map = P.map_words ? (uint16_t *)my : nullptr;
-  const LeafBuf lb{my + map_w, (int *)(my + map_w + LEAF_BUF), (int *)(my + map_w + LEAF_BUF + 32)};
+  const LeafBuf lb{(int *)(my + map_w), (int *)(my + map_w + 32)};
   uint32_t *my_smem = my + map_w + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   if (map)
@@ -1336,7 +1301,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   uint32_t *my = smem + (int64_t)wib * (LEAF_WORDS + A.budget_words);
-  const LeafBuf lb{my, (int *)(my + LEAF_BUF), (int *)(my + LEAF_BUF + 32)};
+  const LeafBuf lb{(int *)my, (int *)(my + 32)};
   uint32_t *my_smem = my + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   Acc128 total{0, 0};
