@@ -95,6 +95,7 @@ typedef struct bc_report {
   double time_level1;            /* s: level-1 pass (time_1hop analogue) */
   double time_enum;              /* s: enumeration (time_2hop analogue) */
   double time_total;             /* s: whole call */
+  int64_t level1_operand_words;  /* BC_FLAG_INSTRUMENT: the level-1 share of operand_words */
 } bc_report;
 
 /* Export ids for bc_export (device structures, for parity tests). */

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
     if (INSTR) {
       atomicAdd(P.ctr + CTR_INTER, inter);
       atomicAdd(P.ctr + CTR_OPW, opw);
+      atomicAdd(P.ctr + CTR_OPW_L1, opw);
       atomicAdd(P.ctr + CTR_MINW, minw);
     }
     if (maxro) atomicMax(P.ctr + CTR_MAXRO, maxro);
@@ -1197,6 +1198,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   out.batches_executed = (s.p_eff >= 2 ? nloc : 0) + (int64_t)h_ctr[CTR_BATCHES];
   out.intersections = (int64_t)h_ctr[CTR_INTER];
   out.operand_words = (int64_t)h_ctr[CTR_OPW];
+  out.level1_operand_words = (int64_t)h_ctr[CTR_OPW_L1];
   out.min_words = (int64_t)h_ctr[CTR_MINW];
   out.time_level1 = t1 * 1e-3;
   out.time_enum = t2 * 1e-3;

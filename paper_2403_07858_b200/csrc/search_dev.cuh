@@ -87,7 +87,7 @@ struct Params {
 
 enum { CTR_ALIVE = 0, CTR_BATCHES, CTR_STOLEN, CTR_INTER, CTR_OPW, CTR_MINW, CTR_MAXRO,
        CTR_MAXSCR, CTR_SPILL, CTR_NEXT, CTR_SUB_USED, CTR_SUB_N, CTR_SUB_NEXT, CTR_SPLIT,
-       CTR_HEAVY, CTR_MAXRO_T, CTR_MAXSCR_T, CTR_COUNT };
+       CTR_HEAVY, CTR_OPW_L1, CTR_COUNT };
 
 struct Info {  // level-1 facts of one task
   int32_t cr, wr, cl, wl;
