@@ -526,7 +526,9 @@ __global__ void sub_keys(const uint32_t *arena, const unsigned long long *index,
   unsigned cr = 0, cl = 0;
   for (int w = 0; w < WR; w++) cr += __popc(rec[4 + w]);
   for (int w = 0; w < WL; w++) cl += __popc(rec[4 + WR + w]);
-  const unsigned long long k = (unsigned long long)cl * cl * (cr ? cr : 1);
+  // candidates below the node ~ |L|^2 |R|, each an AND over the task's WR + WL words
+  const unsigned long long k =
+      (unsigned long long)cl * cl * (cr ? cr : 1) * (unsigned long long)(WR + WL) / 4 + 1;
   key[i] = k > 0xffffffffull ? 0xffffffffu : (uint32_t)k;
   val[i] = index[i];
 }
@@ -1154,8 +1156,30 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
                                                                         info.p, k0.p, v0.p);
                 sort_pairs_desc(k0.p, k1.p, v0.p, v1.p, n_sub, st);
                 A.sub_order = v1.p;
+                if (dt.on) {
+                  uint32_t top[4] = {0, 0, 0, 0};
+                  copy_d2h(top, k1.p, sizeof(uint32_t) * std::min<int64_t>(4, n_sub), st);
+                  const unsigned long long ksum = sum_device(k1.p, n_sub, st);
+                  fprintf(stderr, "[bc search]   sub keys top %u %u %u %u sum %llu\n", top[0], top[1],
+                          top[2], top[3], ksum);
+                }
+                cudaEvent_t k0e, k1e;
+                if (dt.on) {
+                  BC_CUDA(cudaEventCreate(&k0e));
+                  BC_CUDA(cudaEventCreate(&k1e));
+                  BC_CUDA(cudaEventRecord(k0e, st));
+                }
                 if (compact) sub_launch_c1(instr, (unsigned)sblocks, ssmem, st, P, A, n_sub);
                 else sub_launch_c0(instr, (unsigned)sblocks, ssmem, st, P, A, n_sub);
+                if (dt.on) {
+                  BC_CUDA(cudaEventRecord(k1e, st));
+                  BC_CUDA(cudaEventSynchronize(k1e));
+                  float kms = 0;
+                  BC_CUDA(cudaEventElapsedTime(&kms, k0e, k1e));
+                  fprintf(stderr, "[bc search]   sub_kernel %.3f ms (events)\n", kms);
+                  cudaEventDestroy(k0e);
+                  cudaEventDestroy(k1e);
+                }
                 dt.mark("split sub");
                 launches += 3;
               }
