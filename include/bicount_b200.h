@@ -36,7 +36,7 @@ extern "C" {
 #define BC_EOOM (-4)
 #define BC_EOVERFLOW (-5)
 
-#define BC_ABI_VERSION 1
+#define BC_ABI_VERSION 2
 
 /* EngineConfig (engine.py:43-61) plus the device-side knobs. */
 typedef struct bc_config {

@@ -110,7 +110,7 @@ def load():
     global _lib
     if _lib is None:
         L = open_library()
-        if L.bc_abi_version() != 1:
+        if L.bc_abi_version() != 2:
             raise RuntimeError("libbicount_b200.so ABI version mismatch")
         if L.bc_device_count() < 1:
             raise RuntimeError("no CUDA device visible: the B200 path has no CPU fallback")

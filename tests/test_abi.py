@@ -35,15 +35,15 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_device_probe(lib):
-    assert lib.bc_abi_version() == 1
+    assert lib.bc_abi_version() == 2
     assert lib.bc_device_count() >= 0
 
 
 def test_struct_layout_matches_header():
     # bc_config: 8 x int32, then ptr/int64 pairs x 3 -> 32 + 48 = 80 bytes
     assert C.sizeof(_abi.BcConfig) == 80
-    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 = 16 + 16 + 144 + 40
-    assert C.sizeof(_abi.BcReport) == 216
+    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 + 1 i64 = 16 + 16 + 144 + 40 + 8
+    assert C.sizeof(_abi.BcReport) == 224
     text = open(HEADER).read()
     cfg_body = re.search(r"typedef struct bc_config \{(.*?)\} bc_config;", text, re.S).group(1)
     names = re.findall(r"\*?(\w+)\s*(?:,|;)", re.sub(r"/\*.*?\*/", "", cfg_body, flags=re.S))
