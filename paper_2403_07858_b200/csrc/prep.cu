@@ -41,14 +41,18 @@ T d2h_scalar(const T *p, cudaStream_t st) {
 // 2-hop index: one CTA per anchor vertex u (dynamic queue, heaviest first).
 // Counters for ids of the current tile live in shared memory (two u16 per
 // u32 word, or one u32 per id when WIDE), next to a "touched" bitmap with one
-// bit per id.  Increments stop once a counter reaches k (the reads are racy
-// but monotone: a stale read costs one extra increment, at most blockDim per
-// id, which keeps u16 counters exact below k <= 60000).  The first increment
-// of an id sets its touched bit, so the emit phase visits only the touched
-// 32-id words: pass 1 turns each touched word into its kept mask (count >= k,
-// id != u) and clears the counters; pass 2 writes the kept ids in ascending
-// order with a block-wide exclusive scan and clears the bitmap.  Cost per
-// vertex is O(pool + n/32), not O(n).
+// bit per id and a summary bitmap with one bit per touched 32-id word.
+// The wedges u - v - w (v in N(u), w in N(v)) are walked as one flattened
+// range per batch of TH_THREADS neighbours (block scan of the row lengths,
+// owner by bisection in shared memory), so hub rows do not leave the other
+// warps waiting at the barrier.  Increments stop once a counter reaches k (the
+// reads are racy but monotone: a stale read costs one extra increment, at most
+// blockDim per id, which keeps u16 counters exact below k <= 60000).  The first
+// increment of an id sets its touched bit (and, for a word's first id, its
+// summary bit); the summary is compacted into the ascending list of touched
+// words, pass 1 turns each into its kept mask (count >= k, id != u) and clears
+// the counters, pass 2 writes the kept ids in ascending order with a block-wide
+// exclusive scan.  Cost per vertex is O(pool + n/1024), not O(n).
 // ---------------------------------------------------------------------------
 constexpr int TH_THREADS = 512;
 
@@ -58,7 +62,16 @@ __device__ __forceinline__ uint32_t ctr_get(const uint32_t *c, int64_t i) {
   return (c[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
 }
 
-template <bool WIDE>
+// shared-memory words per tile: counters, touched bits, summary bits, touched-word list
+__host__ __device__ __forceinline__ int64_t th_ctr_words(int64_t tile, bool wide) {
+  return wide ? tile : (tile + 1) / 2;
+}
+__host__ __device__ __forceinline__ int64_t th_smem_words(int64_t tile, bool wide) {
+  const int64_t nt = (tile + 31) / 32;
+  return th_ctr_words(tile, wide) + nt + (nt + 31) / 32 + nt;
+}
+
+template <bool WIDE, bool SUMMARY>
 __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
     const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
     const int64_t *__restrict__ boff, const int32_t *__restrict__ bidx,
@@ -72,16 +85,20 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
     typename Scan::TempStorage scan;
     typename Reduce::TempStorage reduce;
   } tmp;
+  __shared__ int64_t s_rstart[TH_THREADS];
+  __shared__ int s_roff[TH_THREADS + 1];
   extern __shared__ uint32_t sm[];
-  const int64_t nctr = WIDE ? tile : (tile + 1) / 2;
+  const int64_t nctr = th_ctr_words(tile, WIDE);
   const int64_t nbits = (tile + 31) / 32;
+  const int64_t nsum = (nbits + 31) / 32;
   uint32_t *ctr = sm;
   uint32_t *touched = sm + nctr;
+  uint32_t *summary = touched + nbits;
+  int *wlist = (int *)(summary + nsum);
   __shared__ int64_t s_u, s_base;
-  __shared__ int s_total;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = TH_THREADS / 32;
-  for (int64_t i = tid; i < nctr + nbits; i += TH_THREADS) sm[i] = 0;
+  __shared__ int s_total, s_nw;
+  const int tid = threadIdx.x;
+  for (int64_t i = tid; i < nctr + nbits + nsum; i += TH_THREADS) sm[i] = 0;
   __syncthreads();
   for (;;) {
     if (tid == 0) {
@@ -96,12 +113,29 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
     for (int ti = 0; ti < ntiles; ti++) {
       const int64_t t0 = (int64_t)ti * tile;
       const int64_t t1 = t0 + tile < n ? t0 + tile : n;
-      // count phase: warp per 1-hop neighbour v, lanes stride N(v)
-      for (int64_t e = e0 + warp; e < e1; e += nwarps) {
-        const int32_t v = __ldg(aidx + e);
-        const int64_t f0 = __ldg(boff + v), f1 = __ldg(boff + v + 1);
-        for (int64_t f = f0 + lane; f < f1; f += 32) {
-          const int64_t w = __ldg(bidx + f);
+      // count phase: the wedges of TH_THREADS neighbours at a time, spread evenly
+      for (int64_t b = e0; b < e1; b += TH_THREADS) {
+        int len = 0;
+        int64_t st = 0;
+        if (b + tid < e1) {
+          const int32_t v = __ldg(aidx + b + tid);
+          st = __ldg(boff + v);
+          len = (int)(__ldg(boff + v + 1) - st);
+        }
+        int off, sum;
+        Scan(tmp.scan).ExclusiveSum(len, off, sum);
+        s_rstart[tid] = st;
+        s_roff[tid] = off;
+        if (tid == 0) s_roff[TH_THREADS] = sum;
+        __syncthreads();
+        for (int pos = tid; pos < sum; pos += TH_THREADS) {
+          int lo = 0, hi = TH_THREADS - 1;  // last row whose offset is <= pos
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_roff[mid] <= pos) lo = mid;
+            else hi = mid - 1;
+          }
+          const int64_t w = __ldg(bidx + s_rstart[lo] + (pos - s_roff[lo]));
           if (w < t0 || w >= t1) continue;
           const int64_t l = w - t0;
           bool first;
@@ -113,29 +147,52 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
             if (((((volatile uint32_t *)ctr)[l >> 1] >> sh) & 0xffffu) >= k) continue;
             first = ((atomicAdd(&ctr[l >> 1], 1u << sh) >> sh) & 0xffffu) == 0;
           }
-          if (first) atomicOr(&touched[l >> 5], 1u << (l & 31));
+          if (first) {
+            const uint32_t old = atomicOr(&touched[l >> 5], 1u << (l & 31));
+            if (SUMMARY && old == 0) atomicOr(&summary[l >> 10], 1u << ((l >> 5) & 31));
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
+      // the touched words, ascending: compaction of the summary bitmap (SUMMARY, for
+      // vertices whose pool is small against the tile), else every word of the tile
+      int nw = 0;
+      const int64_t ntw = (t1 - t0 + 31) / 32;
+      if (!SUMMARY) nw = (int)ntw;
+      for (int64_t r0 = 0; SUMMARY && r0 < nsum; r0 += TH_THREADS) {
+        const int64_t si = r0 + tid;
+        uint32_t sw = si < nsum ? summary[si] : 0u;
+        int off, round;
+        Scan(tmp.scan).ExclusiveSum(__popc(sw), off, round);
+        if (sw) summary[si] = 0;
+        int o = nw + off;
+        while (sw) {
+          const int bb = __ffs(sw) - 1;
+          sw &= sw - 1;
+          wlist[o++] = (int)(si * 32 + bb);
+        }
+        nw += round;
+        __syncthreads();
+      }
       // pass 1: touched words -> kept masks, counters cleared
-      const int64_t nt = (t1 - t0 + 31) / 32;
       int mine = 0;
-      for (int64_t wi = tid; wi < nt; wi += TH_THREADS) {
-        uint32_t t = touched[wi], km = 0;
-        if (!t) continue;
-        uint32_t m = t;
+      for (int i = tid; i < nw; i += TH_THREADS) {
+        const int64_t wi = SUMMARY ? wlist[i] : i;
+        const uint32_t t = touched[wi];
+        if (!SUMMARY && !t) continue;
+        uint32_t km = 0, m = t;
         while (m) {
-          const int b = __ffs(m) - 1;
+          const int bb = __ffs(m) - 1;
           m &= m - 1;
-          const int64_t l = wi * 32 + b;
-          if (ctr_get<WIDE>(ctr, l) >= k && t0 + l != u) km |= 1u << b;
+          const int64_t l = wi * 32 + bb;
+          if (ctr_get<WIDE>(ctr, l) >= k && t0 + l != u) km |= 1u << bb;
         }
         if (WIDE) {
           m = t;
           while (m) {
-            const int b = __ffs(m) - 1;
+            const int bb = __ffs(m) - 1;
             m &= m - 1;
-            ctr[wi * 32 + b] = 0;
+            ctr[wi * 32 + bb] = 0;
           }
         } else {
           for (int h = 0; h < 16; h++)
@@ -148,9 +205,9 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
       if (tid == 0) {
         int64_t base = -1;
         if (kept) {
-          unsigned long long b = atomicAdd(out_used, (unsigned long long)kept);
-          if ((int64_t)b + kept > out_cap) atomicExch(overflow, 1);
-          else base = (int64_t)b;
+          unsigned long long bq = atomicAdd(out_used, (unsigned long long)kept);
+          if ((int64_t)bq + kept > out_cap) atomicExch(overflow, 1);
+          else base = (int64_t)bq;
         }
         s_base = base;
         s_total = kept;
@@ -163,25 +220,26 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
       // pass 2: ordered emit of the kept ids, bitmap cleared
       int64_t pos = 0;
       if (s_total) {
-        for (int64_t r0 = 0; r0 < nt; r0 += TH_THREADS) {
-          const int64_t wi = r0 + tid;
-          uint32_t km = wi < nt ? touched[wi] : 0u;
+        for (int r0 = 0; r0 < nw; r0 += TH_THREADS) {
+          const int i = r0 + tid;
+          const int64_t wi = i < nw ? (SUMMARY ? wlist[i] : i) : 0;
+          uint32_t km = i < nw ? touched[wi] : 0u;
           int off, round;
           Scan(tmp.scan).ExclusiveSum(__popc(km), off, round);
-          if (km) {
-            touched[wi] = 0;
-            if (base >= 0) {
-              int64_t o = base + pos + off;
-              while (km) {
-                const int b = __ffs(km) - 1;
-                km &= km - 1;
-                out_ids[o++] = (int32_t)(t0 + wi * 32 + b);
-              }
+          if (i < nw) touched[wi] = 0;
+          if (km && base >= 0) {
+            int64_t o = base + pos + off;
+            while (km) {
+              const int bb = __ffs(km) - 1;
+              km &= km - 1;
+              out_ids[o++] = (int32_t)(t0 + wi * 32 + bb);
             }
           }
           pos += round;
           __syncthreads();
         }
+      } else {
+        for (int i = tid; i < nw; i += TH_THREADS) touched[SUMMARY ? wlist[i] : i] = 0;
       }
       __syncthreads();
     }
@@ -198,7 +256,7 @@ __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long tot = 0;
+  unsigned long long tot = 0, ptot = 0;
   for (int64_t u = gw; u < n; u += nw) {
     unsigned long long pool = 0;
     for (int64_t e = aoff[u] + lane; e < aoff[u + 1]; e += 32) {
@@ -208,8 +266,10 @@ __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__
     pool = warp_sum(pool);
     const unsigned long long b = pool / k;
     tot += b < (unsigned long long)(n - 1) ? b : (unsigned long long)(n - 1);
+    ptot += pool;
   }
   if (lane == 0 && tot) atomicAdd(out, tot);
+  if (lane == 0 && ptot) atomicAdd(out + 1, ptot);
 }
 
 // vertices by descending degree (LPT order for the 2-hop CTAs)
@@ -522,18 +582,14 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     int smem_optin = 0;
     BC_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g.device));
     // counters + touched bitmap per tile id: 2 B + 1/8 B (u16) or 4 B + 1/8 B (u32)
-    const int64_t budget_bits = (int64_t)(smem_optin - 8192) * 8;
-    int64_t max_tile = wide ? budget_bits / 33 : budget_bits / 17;
+    // counters (16 or 32 bits) + touched bit + touched-word list (32 bits per word) + summary
+    const int64_t budget_bits = (int64_t)(smem_optin - 16384) * 8;
+    int64_t max_tile = wide ? budget_bits / 34 : budget_bits / 18;
     max_tile &= ~int64_t(63);
     ntiles = (int)((n + max_tile - 1) / max_tile);
     tile = (n + ntiles - 1) / ntiles;
     tile = (tile + 63) & ~int64_t(63);
-    const size_t smem = (size_t)((wide ? tile : (tile + 1) / 2) + (tile + 31) / 32) * 4;
-    auto kern = wide ? twohop_kernel<true> : twohop_kernel<false>;
-    BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH_THREADS, smem));
-    if (per_sm < 1) per_sm = 1;
+    const size_t smem = (size_t)th_smem_words(tile, wide) * 4;
     // LPT vertex order: descending anchor degree
     DBuf<unsigned long long> keys, keys2;
     keys.alloc(n, st);
@@ -557,13 +613,24 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     DBuf<int> ctrs;  // [0] next vertex, [1] overflow
     DBuf<unsigned long long> used;
     ctrs.alloc(2, st);
-    used.alloc(1, st);
+    used.alloc(2, st);
     used.zero();
     twohop_bound<<<warp_blocks(n, sms), 256, 0, st>>>(s.aoff, s.aidx, s.boff, n, k, used.p);
     BC_CHECK_LAUNCH();
     L++;
-    int64_t cap = std::min<int64_t>((int64_t)d2h_scalar(used.p, st), int64_t(1) << 31);
+    unsigned long long hb[2];
+    copy_d2h(hb, used.p, sizeof hb, st);
+    BC_CUDA(cudaStreamSynchronize(st));
+    int64_t cap = std::min<int64_t>((int64_t)hb[0], int64_t(1) << 31);
     cap = std::max<int64_t>(cap, 1);
+    // touched-word lists when a vertex's pool is small against the tile's words
+    const bool summary = (double)hb[1] / (double)n < (double)((tile + 31) / 32);
+    auto kern = wide ? (summary ? twohop_kernel<true, true> : twohop_kernel<true, false>)
+                     : (summary ? twohop_kernel<false, true> : twohop_kernel<false, false>);
+    BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH_THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
     for (int attempt = 0; attempt < 2; attempt++) {
       und_ids.alloc(cap, st);
       ctrs.zero();

@@ -1,7 +1,10 @@
 """Summarise an ncu launch-list CSV (gpu__time_duration + DRAM/L2 bytes per launch):
 per kernel name, launches, total ms, share, DRAM and L2 bytes."""
 import csv
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
