@@ -823,10 +823,15 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
                                     long long limit = LLONG_MAX) {
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL, p_eff = P.p_eff;
-  long long work = expand<INSTR, LAZY>(P, f, d, start, map, lb, acc, tl, ph_);
-  if (work > limit) return false;
+  long long work = 0;
   int level = start;
-  while (level >= start) {
+  bool fresh = true;  // one expand call site: the kernel stays small (I-cache)
+  for (;;) {
+    if (fresh) {
+      work += expand<INSTR, LAZY>(P, f, d, level, map, lb, acc, tl, ph_);
+      if (work > limit) return false;
+      fresh = false;
+    }
     const int li = level - 1;
     if (level + 1 < p_eff - 2 && f.cur[li] < f.ns[li]) {
       const int u = f.surv[li * f.surv_cap + f.cur[li]];
@@ -841,9 +846,9 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
       for (int w = lane; w < WL; w += 32) f.setL[(li + 1) * WL + w] = f.setL[li * WL + w] & rl[w];
       __syncwarp();
       level++;
-      work += expand<INSTR, LAZY>(P, f, d, level, map, lb, acc, tl, ph_);
-      if (work > limit) return false;
+      fresh = true;
     } else {
+      if (level == start) break;
       level--;
     }
   }
@@ -1281,8 +1286,10 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
         clear_map(map, f, d);
         continue;
       }
+    } else if (LAZY) {  // p_eff = 4: level 1's children are the leaf-parents, no descent
+      expand<INSTR, true>(P, f, d, 1, map, lb, acc, tl, ph_);
     } else {
-      dfs<INSTR, LAZY>(P, f, d, 1, map, lb, acc, tl, nullptr, ph_);
+      dfs<INSTR, false>(P, f, d, 1, map, lb, acc, tl, nullptr, ph_);
     }
     PH_MARK(4);
     clear_map(map, f, d);
