@@ -479,6 +479,11 @@ __global__ void rows_cost(const Info *__restrict__ info, int64_t nloc, int strid
   }
 }
 
+__global__ void alive_flags(const uint32_t *cost, int64_t n, uint8_t *flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = cost[i] != 0;
+}
+
 __global__ void gather_keys(const int32_t *ids, int64_t n, const uint32_t *cost, uint32_t *out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = cost[ids[i]];
@@ -1008,6 +1013,29 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             EnumArgs B = A;
             B.q0 = 0;
             B.q1 = n_alive;
+            // triage drains the alive tasks in emission order: the tasks of one root are
+            // adjacent, so their C_R1 members' rows (all in N(root)) are re-read from L2
+            DBuf<int32_t> tq;
+            if (!env_int("BC_TRIAGE_LPT", 0)) {
+              DBuf<int32_t> ids;
+              DBuf<uint8_t> flags;
+              DBuf<int64_t> nsel;
+              ids.alloc(nloc, st);
+              flags.alloc(nloc, st);
+              tq.alloc(nloc, st);
+              nsel.alloc(1, st);
+              iota32<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(ids.p, nloc);
+              alive_flags<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(cost.p, nloc, flags.p);
+              size_t tmp = 0;
+              BC_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, ids.p, flags.p, tq.p, nsel.p, nloc,
+                                                 st));
+              DBuf<char> tb;
+              tb.alloc(tmp, st);
+              BC_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, ids.p, flags.p, tq.p, nsel.p, nloc,
+                                                 st));
+              B.queue = tq.p;
+              launches += 3;
+            }
             B.budget_words = budget;
             B.triage = T;
             B.triage_work = env_int("BC_TRIAGE_WORK", 1 << 16);
