@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
 // drawn from an atomic queue.  dir2(r) membership and slot (= position in
 // dir2(r) = task offset from troot[r]) come from a per-warp shared-memory
 // bitmap over anchor ids plus a u16 prefix per word (n <= 65536), else from a
-// binary search of dir2(r).  Pass 1 counts hits per (unit, slot); a column
-// scan turns them into per-task list offsets and per-unit cursors; pass 2
-// appends, 32 neighbours per round, ranking same-slot hits by lane with a
-// per-warp hit mask so every list comes out sorted.
+// binary search of dir2(r).  The rows of 32 neighbours are walked as one
+// flattened list over the lanes (four gathers in flight per lane).  Pass 1
+// counts hits per (unit, slot); a column scan turns them into per-task list
+// offsets and per-unit cursors; pass 2 appends, ranking the same-slot hits of a
+// round by lane (__match_any_sync) so every list comes out sorted.
 // ---------------------------------------------------------------------------
 constexpr int L1_CH = 1024;
 constexpr int L1_THREADS = 128;
@@ -214,8 +215,6 @@ struct L1Args {
   int map_words;            // bitmap words per warp (0 = binary search)
   int shard, nshards;
   int32_t *lists;           // pass 2
-  uint32_t *masks;          // pass 2: per-warp hit masks [mask_stride]
-  int64_t mask_stride;
   unsigned long long *next;
 };
 
@@ -268,7 +267,6 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
   if (bits)
     for (int i = lane; i < mw; i += 32) bits[i] = 0;
   __syncwarp();
-  uint32_t *mask = FILL ? A.masks + gwarp * A.mask_stride : nullptr;
   for (;;) {
     long long u = 0;
     if (lane == 0) u = (long long)atomicAdd(A.next, 1ull);
@@ -283,46 +281,63 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
     unsigned long long *col = A.aux + A.ubase[r] + (int64_t)c * m.D;
     const int64_t e0 = A.aoff[r] + (int64_t)c * L1_CH;
     const int64_t e1 = min(A.aoff[r + 1], e0 + L1_CH);
+    // the rows of 32 neighbours at a time as one flattened list over the lanes; rounds of
+    // 32 consecutive positions keep the owners (hence v) ascending across the lanes
     for (int64_t base = e0; base < e1; base += 32) {
       const int64_t e = base + lane;
       int32_t v = 0;
-      int64_t f0 = 0, f1 = 0;
+      int64_t st = 0;
+      int len = 0;
       if (e < e1) {
         v = __ldg(A.aidx + e);
-        f0 = __ldg(A.boff + v);
-        f1 = __ldg(A.boff + v + 1);
+        st = __ldg(A.boff + v);
+        len = (int)(__ldg(A.boff + v + 1) - st);
       }
-      if (!FILL) {
-        for (int64_t f = f0; f < f1; f++) {
-          const int k = m.slot(__ldg(A.bidx + f));
-          if (k >= 0 && (T0 + k) % A.nshards == A.shard) atomicAdd(col + k, 1ull);
-        }
-      } else {
-        // (a) hit masks, (b) ranked writes, (c) the lowest hitter advances the cursor
-        for (int64_t f = f0; f < f1; f++) {
-          const int k = m.slot(__ldg(A.bidx + f));
-          if (k >= 0 && (T0 + k) % A.nshards == A.shard) atomicOr(mask + k, 1u << lane);
-        }
-        __syncwarp();
-        for (int64_t f = f0; f < f1; f++) {
-          const int k = m.slot(__ldg(A.bidx + f));
-          if (k >= 0 && (T0 + k) % A.nshards == A.shard) {
-            const uint32_t mk = *(volatile uint32_t *)(mask + k);
-            A.lists[col[k] + __popc(mk & lanemask_lt())] = v;
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int excl = incl - len;
+      const int T = __shfl_sync(FULL, incl, 31);
+      constexpr int U = 4;  // gathers in flight per lane
+      for (int r0 = 0; r0 < T; r0 += 32 * U) {
+        int ks[U];
+        int32_t vs[U];
+#pragma unroll
+        for (int uu = 0; uu < U; uu++) {
+          const int pos = r0 + 32 * uu + lane;
+          int sl = 0;
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1) {
+            const int cc = sl + step;
+            const int ee = __shfl_sync(FULL, excl, cc < 32 ? cc : 31);
+            if (cc < 32 && ee <= pos) sl = cc;
           }
+          const int64_t so = __shfl_sync(FULL, st, sl);
+          const int eo = __shfl_sync(FULL, excl, sl);
+          vs[uu] = __shfl_sync(FULL, v, sl);
+          ks[uu] = pos < T ? __ldg(A.bidx + so + (pos - eo)) : -1;
         }
-        __syncwarp();
-        for (int64_t f = f0; f < f1; f++) {
-          const int k = m.slot(__ldg(A.bidx + f));
-          if (k >= 0 && (T0 + k) % A.nshards == A.shard) {
-            const uint32_t mk = *(volatile uint32_t *)(mask + k);
-            if (mk && __ffs(mk) - 1 == lane) {
-              col[k] += __popc(mk);
-              mask[k] = 0;
+#pragma unroll
+        for (int uu = 0; uu < U; uu++) {
+          int k = ks[uu] >= 0 ? m.slot(ks[uu]) : -1;
+          if (k >= 0 && (T0 + k) % A.nshards != A.shard) k = -1;
+          if (!FILL) {
+            if (k >= 0) atomicAdd(col + k, 1ull);
+          } else {
+            // same-slot hits of this round, ranked by lane (= by ascending v)
+            const unsigned grp = __match_any_sync(FULL, k >= 0 ? k : -1 - lane);
+            const unsigned long long c0 = k >= 0 ? col[k] : 0ull;
+            __syncwarp();
+            if (k >= 0) {
+              A.lists[c0 + __popc(grp & lanemask_lt())] = vs[uu];
+              if (((grp >> lane) >> 1) == 0) col[k] = c0 + __popc(grp);
             }
+            __syncwarp();
           }
         }
-        __syncwarp();
       }
     }
     __syncwarp();  // lanes still probing the map must finish before it is cleared
@@ -817,11 +832,6 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       l1_cursors<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
           s.tasks.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p, s.dir_off.p,
           l1_roff.p, aux.p);
-      DBuf<uint32_t> masks;
-      A1.mask_stride = (int64_t)std::max<unsigned long long>(maxD, 1);
-      masks.alloc((size_t)l1blocks * l1w * A1.mask_stride, st);
-      masks.zero();
-      A1.masks = masks.p;
       A1.lists = l1_lists.p;
       A1.next = nxt.p + 1;
       dt.mark("l1 offsets");
