@@ -549,6 +549,8 @@ __device__ __forceinline__ unsigned node_batches(const Params &P, unsigned ncand
 }
 
 // Per-warp shared-memory staging of (leaf-parent slot, leaf) pairs.
+constexpr int RP_WORDS = 2;  // leaf-parent R' words kept in registers
+
 struct LeafBuf {
   int *wr;     // [32]: C_R word count of each slot's leaf-parent
   int *ncand;  // [32]: leaves of each slot's leaf-parent (batch accounting)
@@ -563,7 +565,8 @@ constexpr int LEAF_WORDS = 64;  // per-warp leaf-parent bookkeeping in shared me
 template <bool INSTR>
 __device__ __forceinline__ void eval_leaves(const Params &P, const Frame &f, const Dims &d,
                                             const uint32_t *R, const int *slot_u, int slot,
-                                            uint32_t v, int pre, uint32_t m, int wr, Acc128 &acc,
+                                            uint32_t v, int pre, uint32_t m, int wr,
+                                            const uint32_t (&rp)[RP_WORDS], Acc128 &acc,
                                             Tally &tl) {
   const int lane = lane_id();
   const int cnt = __popc(m);
@@ -589,13 +592,25 @@ __device__ __forceinline__ void eval_leaves(const Params &P, const Frame &f, con
     const uint32_t vo = __shfl_sync(FULL, v, o), mo = __shfl_sync(FULL, m, o);
     const int po = __shfl_sync(FULL, pre, o), eo = __shfl_sync(FULL, excl, o);
     const int wro = INSTR ? __shfl_sync(FULL, wr, o) : 0;
+    // R & rowR[u] of the leaf-parent, held in its lane's registers when it is short
+    uint32_t pr[RP_WORDS];
+#pragma unroll
+    for (int x = 0; x < RP_WORDS; x++) pr[x] = x < WR ? __shfl_sync(FULL, rp[x], so) : 0u;
     if (k < total) {
       const int b = (int)__fns(mo, 0, k - eo + 1);
       const int w = po + __popc(vo & ((1u << b) - 1u));
-      const uint32_t *ru = rowR_of(f, d, slot_u[so]), *rw = rowR_of(f, d, w);
+      const uint32_t *rw = rowR_of(f, d, w);
       int c = 0;
-      if (rw)
-        for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
+      if (rw) {
+        if (WR <= RP_WORDS) {
+#pragma unroll
+          for (int x = 0; x < RP_WORDS; x++)
+            if (x < WR) c += __popc(pr[x] & rw[x]);
+        } else {
+          const uint32_t *ru = rowR_of(f, d, slot_u[so]);
+          for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
+        }
+      }
       if (INSTR) {
         tl.inter++;
         tl.opw += wro + f.adjw[w];
@@ -626,7 +641,11 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     const int i = base + lane;
     const bool act = i < n;
     const int u = act ? list[i] : 0;
-    const int wr = act ? lane_words(R, rowR_of(f, d, u), f.r_last, WR) : 0;
+    const uint32_t *ru_mine = act ? rowR_of(f, d, u) : nullptr;
+    const int wr = act ? lane_words(R, ru_mine, f.r_last, WR) : 0;
+    uint32_t rp[RP_WORDS];
+#pragma unroll
+    for (int x = 0; x < RP_WORDS; x++) rp[x] = act && x < WR ? R[x] & ru_mine[x] : 0u;
     lb.wr[lane] = wr;
     lb.ncand[lane] = 0;
     __syncwarp();
@@ -671,7 +690,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
             if (m) atomicAdd(&lb.ncand[sl], __popc(m));
           }
         }
-        eval_leaves<INSTR>(P, f, d, R, list + base, sl, v, pre, m, lb.wr[sl], acc, tl);
+        eval_leaves<INSTR>(P, f, d, R, list + base, sl, v, pre, m, lb.wr[sl], rp, acc, tl);
       }
     } else {
       int ncand = 0;
@@ -680,7 +699,8 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
         uint32_t m = 0;
         if (act && x < WL) m = Ls[x] & rl[x];
         ncand += __popc(m);
-        eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, acc, tl);
+        eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, rp, acc,
+                           tl);
       }
       lb.ncand[lane] = ncand;
     }
