@@ -119,8 +119,16 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
         int64_t st = 0;
         if (b + tid < e1) {
           const int32_t v = __ldg(aidx + b + tid);
-          st = __ldg(boff + v);
-          len = (int)(__ldg(boff + v + 1) - st);
+          int64_t lo = __ldg(boff + v), hi = __ldg(boff + v + 1);
+          const int64_t end = hi;
+          const int32_t key = (int32_t)(u >= t0 ? u + 1 : t0);  // first id counted: > u, in tile
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(bidx + mid) < key) lo = mid + 1;
+            else hi = mid;
+          }
+          st = lo;
+          len = (int)(end - lo);
         }
         int off, sum;
         Scan(tmp.scan).ExclusiveSum(len, off, sum);
@@ -243,7 +251,7 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
       }
       __syncthreads();
     }
-    if (tid == 0) und_size[u] = total;
+    if (tid == 0) und_size[u] = total;  // the upper part |{w > u}|; lower parts added later
     __syncthreads();
   }
 }
@@ -270,6 +278,67 @@ __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__
   }
   if (lane == 0 && tot) atomicAdd(out, tot);
   if (lane == 0 && ptot) atomicAdd(out + 1, ptot);
+}
+
+// The 2-hop relation is symmetric (|N(u) & N(w)| both ways), so the kernel above
+// counts only w > u: half the wedges.  und(u) = {w < u : u in up(w)} ++ up(u).
+// lower_counts: |{w < u : u in up(w)}| per u (warp per w walking up(w)'s tiles).
+__global__ void lower_counts(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
+                             int ntiles, const int32_t *__restrict__ up_ids, int64_t n,
+                             int64_t *__restrict__ cnt_low) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = gw; w < n; w += nw)
+    for (int ti = 0; ti < ntiles; ti++) {
+      const int64_t st = seg_start[w * ntiles + ti];
+      const int32_t ln = seg_len[w * ntiles + ti];
+      for (int32_t i = lane; i < ln; i += 32) atomicAdd((unsigned long long *)(cnt_low + up_ids[st + i]), 1ull);
+    }
+}
+
+// und lists: up(u) copied after the lower part; lower entries u -> und(x) appended
+// (unordered) to the lower part of x, sorted afterwards
+__global__ void und_fill(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
+                         int ntiles, const int32_t *__restrict__ up_ids, int64_t n,
+                         const int64_t *__restrict__ und_off, const int64_t *__restrict__ cnt_low,
+                         unsigned long long *__restrict__ cur_low, int32_t *__restrict__ low_buf,
+                         int32_t *__restrict__ und_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n; u += nw) {
+    int64_t pos = und_off[u] + cnt_low[u];
+    for (int ti = 0; ti < ntiles; ti++) {
+      const int64_t st = seg_start[u * ntiles + ti];
+      const int32_t ln = seg_len[u * ntiles + ti];
+      for (int32_t i = lane; i < ln; i += 32) {
+        const int32_t x = up_ids[st + i];
+        und_out[pos + i] = x;
+        low_buf[und_off[x] + (int64_t)atomicAdd(cur_low + x, 1ull)] = (int32_t)u;
+      }
+      pos += ln;
+    }
+  }
+}
+
+__global__ void add_sizes(const int64_t *__restrict__ a, const int64_t *__restrict__ b, int64_t n,
+                          int64_t *__restrict__ out, int64_t *__restrict__ low_end,
+                          const int64_t *__restrict__ off) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    out[i] = a[i] + b[i];
+    if (off) low_end[i] = off[i] + b[i];
+  }
+}
+
+__global__ void as_segments(const int64_t *__restrict__ off, const int64_t *__restrict__ size,
+                            int64_t n, int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    seg_start[i] = off[i];
+    seg_len[i] = (int32_t)size[i];
+  }
 }
 
 // vertices by descending degree (LPT order for the 2-hop CTAs)
@@ -643,10 +712,53 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       L++;
       int ovf = d2h_scalar(ctrs.p + 1, st);
       unsigned long long need = d2h_scalar(used.p, st);
-      s.und_pairs = (int64_t)need;
       if (!ovf) break;
       if (attempt == 1) throw Error(BC_ECUDA, "2-hop output overflow after exact resize");
       cap = (int64_t)need;
+    }
+    // symmetrise: und(u) = lower part (sorted) ++ up(u)
+    {
+      DBuf<int64_t> low, size, off, low_end;
+      DBuf<unsigned long long> cur;
+      low.alloc(n, st);
+      low.zero();
+      size.alloc(n + 1, st);
+      size.zero();
+      off.alloc(n + 1, st);
+      low_end.alloc(n, st);
+      cur.alloc(n, st);
+      cur.zero();
+      lower_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+                                                        n, low.p);
+      add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, low.p, n, size.p, nullptr,
+                                                     nullptr);
+      exclusive_scan(size.p, off.p, n + 1, st);
+      s.und_pairs = d2h_scalar(off.p + n, st);
+      add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, low.p, n, s.und_size.p,
+                                                     low_end.p, off.p);
+      DBuf<int32_t> low_buf, und_full;
+      low_buf.alloc(s.und_pairs ? s.und_pairs : 1, st);
+      und_full.alloc(s.und_pairs ? s.und_pairs : 1, st);
+      und_fill<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p, n,
+                                                    off.p, low.p, cur.p, low_buf.p, und_full.p);
+      BC_CHECK_LAUNCH();
+      if (s.und_pairs > 0) {  // the lower parts, ascending (the upper parts already are)
+        size_t tmp = 0;
+        BC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, low_buf.p, und_full.p,
+                                                    s.und_pairs, n, off.p, low_end.p, st));
+        DBuf<char> t;
+        t.alloc(tmp, st);
+        BC_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, low_buf.p, und_full.p, s.und_pairs,
+                                                    n, off.p, low_end.p, st));
+      }
+      seg_start.alloc(n, st);
+      seg_len.alloc(n, st);
+      as_segments<<<blocks_for(n, 256), 256, 0, st>>>(off.p, s.und_size.p, n, seg_start.p,
+                                                      seg_len.p);
+      BC_CHECK_LAUNCH();
+      und_ids = std::move(und_full);
+      ntiles = 1;
+      L += 7;
     }
   } else {
     s.und_pairs = 0;
