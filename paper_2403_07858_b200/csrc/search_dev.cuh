@@ -499,11 +499,12 @@ __device__ __forceinline__ int words_touched(const uint32_t *set, const uint32_t
 // and never carries out of a field, so the touched fields are
 // popc(((X & ~last) + ~last | X) & last).
 __device__ __forceinline__ int lane_words(const uint32_t *R, const uint32_t *ru,
-                                          const uint32_t *last, int W) {
+                                          const uint32_t *last, int W,
+                                          const uint32_t *ru2 = nullptr) {
   int c = 0;
   unsigned long long carry = 0;
   for (int w = 0; w < W; w++) {
-    const uint32_t x = R[w] & ru[w], L = last[w];
+    const uint32_t x = R[w] & ru[w] & (ru2 ? ru2[w] : FULL), L = last[w];
     const unsigned long long sum = (unsigned long long)(x & ~L) + (unsigned long long)(~L) + carry;
     carry = sum >> 32;
     c += __popc(((uint32_t)sum | x) & L);
@@ -554,8 +555,9 @@ constexpr int RP_WORDS = 2;  // leaf-parent R' words kept in registers
 struct LeafBuf {
   int *wr;     // [32]: C_R word count of each slot's leaf-parent
   int *ncand;  // [32]: leaves of each slot's leaf-parent (batch accounting)
+  int *pu, *pw;  // [64] each: (child, grandchild) leaf-parent pairs awaiting evaluation
 };
-constexpr int LEAF_WORDS = 64;  // per-warp leaf-parent bookkeeping in shared memory
+constexpr int LEAF_WORDS = 64 + 128;  // per-warp leaf-parent bookkeeping in shared memory
 
 // Evaluate one round of leaves (engine.py:342-347): lane i offers the present bits m
 // of an HTB-style word (v, pre) for leaf-parent `slot`; all offered leaves, as one
@@ -632,7 +634,7 @@ template <bool INSTR, bool LAZY>
 __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, const Dims &d,
                                              int level, const int *list, int n,
                                              const uint16_t *map, const LeafBuf &lb, Acc128 &acc,
-                                             Tally &tl) {
+                                             Tally &tl, const int *list2 = nullptr) {
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL;
   const uint32_t *R = f.setR + (level - 1) * WR;
@@ -642,10 +644,12 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     const bool act = i < n;
     const int u = act ? list[i] : 0;
     const uint32_t *ru_mine = act ? rowR_of(f, d, u) : nullptr;
-    const int wr = act ? lane_words(R, ru_mine, f.r_last, WR) : 0;
+    const uint32_t *ru2 = act && list2 ? rowR_of(f, d, list2[i]) : nullptr;
+    const int wr = act ? lane_words(R, ru_mine, f.r_last, WR, ru2) : 0;
     uint32_t rp[RP_WORDS];
 #pragma unroll
-    for (int x = 0; x < RP_WORDS; x++) rp[x] = act && x < WR ? R[x] & ru_mine[x] : 0u;
+    for (int x = 0; x < RP_WORDS; x++)
+      rp[x] = act && x < WR ? R[x] & ru_mine[x] & (ru2 ? ru2[x] : FULL) : 0u;
     lb.wr[lane] = wr;
     lb.ncand[lane] = 0;
     __syncwarp();
@@ -695,9 +699,10 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     } else {
       int ncand = 0;
       const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL;
+      const uint32_t *rl2 = act && list2 ? rowL_of(f, d, list2[i]) : nullptr;
       for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
         uint32_t m = 0;
-        if (act && x < WL) m = Ls[x] & rl[x];
+        if (act && x < WL) m = Ls[x] & rl[x] & (rl2 ? rl2[x] : FULL);
         ncand += __popc(m);
         eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, rp, acc,
                            tl);
@@ -707,6 +712,133 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     if (act) tl.batches += node_batches(P, (unsigned)lb.ncand[lane], wr, 0, true);
     __syncwarp();
   }
+}
+
+// Expand all children of the node at `level` at once when its grandchildren are
+// leaf-parents (engine.py:315-374 applied to each child): a child u has
+// R_u = R & rowR[u] (<= RP_WORDS words, in its lane's registers) and
+// L_u = L & rowL[u]; the candidates w of 32 children are one flattened list over
+// the lanes (owner bisection as in eval_leaves), each tested for
+// |R_u & rowR[w]| >= q and |L_u & rowL[w]| >= p - level - 3, and the surviving
+// (u, w) leaf-parents are finished 32 at a time (leaf_parents with pairs).
+// Per-node batch accounting and intersection tallies are those of expand.
+template <bool INSTR>
+__device__ __forceinline__ int expand_children(const Params &P, const Frame &f, const Dims &d,
+                                               int level, const LeafBuf &lb, Acc128 &acc,
+                                               Tally &tl) {
+  const int lane = lane_id();
+  const int WR = d.WR, WL = d.WL;
+  const int li = level - 1;
+  const uint32_t *R = f.setR + li * WR;
+  const uint32_t *Ls = f.setL + li * WL;
+  const int n = f.ns[li];
+  const int *kids = f.surv + li * f.surv_cap;
+  const int need_g = P.p_eff - level - 3;  // prune_keep at level + 2
+  int work = 0, fill = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const bool act = i < n;
+    const int u = act ? kids[i] : 0;
+    const uint32_t *ru = act ? rowR_of(f, d, u) : nullptr;
+    const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL;
+    uint32_t rp[RP_WORDS];
+#pragma unroll
+    for (int x = 0; x < RP_WORDS; x++) rp[x] = act && x < WR ? R[x] & ru[x] : 0u;
+    const int wr_u = act ? lane_words(R, ru, f.r_last, WR) : 0;
+    const int wl_u = act ? lane_words(Ls, rl, f.l_last, WL) : 0;
+    int ncand_u = 0;
+    for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
+      const uint32_t m = act && x < WL ? Ls[x] & rl[x] : 0u;
+      ncand_u += __popc(m);
+      const int cnt = __popc(m);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int excl = incl - cnt;
+      const int total = __shfl_sync(FULL, incl, 31);
+      for (int r0 = 0; r0 < total; r0 += 32) {
+        const int k = r0 + lane;
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int c = o + step;
+          const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
+          if (c < 32 && e <= k) o = c;
+        }
+        const uint32_t mo = __shfl_sync(FULL, m, o);
+        const int eo = __shfl_sync(FULL, excl, o);
+        const int uo = __shfl_sync(FULL, u, o);
+        const int wro = INSTR ? __shfl_sync(FULL, wr_u, o) : 0;
+        const int wlo = INSTR ? __shfl_sync(FULL, wl_u, o) : 0;
+        uint32_t pr[RP_WORDS];
+#pragma unroll
+        for (int x2 = 0; x2 < RP_WORDS; x2++) pr[x2] = x2 < WR ? __shfl_sync(FULL, rp[x2], o) : 0u;
+        bool keep = false;
+        int w = 0;
+        if (k < total) {
+          w = x * 32 + (int)__fns(mo, 0, k - eo + 1);
+          const uint32_t *rw = rowR_of(f, d, w);
+          int cr = 0;
+          if (rw) {
+#pragma unroll
+            for (int x2 = 0; x2 < RP_WORDS; x2++)
+              if (x2 < WR) cr += __popc(pr[x2] & rw[x2]);
+          }
+          if (INSTR) {
+            tl.inter++;
+            tl.opw += wro + f.adjw[w];
+            tl.minw += wro < f.adjw[w] ? wro : f.adjw[w];
+          }
+          if (cr >= P.q_eff) {
+            if (INSTR) {
+              tl.inter++;
+              tl.opw += wlo + f.dirw[w];
+              tl.minw += wlo < f.dirw[w] ? wlo : f.dirw[w];
+            }
+            const uint32_t *rlo = rowL_of(f, d, uo), *rlw = rowL_of(f, d, w);
+            int cl = 0;
+            for (int x2 = 0; x2 < WL; x2++) cl += __popc(Ls[x2] & rlo[x2] & rlw[x2]);
+            keep = cl >= need_g;
+          }
+        }
+        const unsigned km = __ballot_sync(FULL, keep);
+        if (keep) {
+          const int at = fill + __popc(km & lanemask_lt());
+          lb.pu[at] = uo;
+          lb.pw[at] = w;
+        }
+        fill += __popc(km);
+        __syncwarp();
+        if (fill >= 32) {  // finish 32 leaf-parents, keep the rest
+          leaf_parents<INSTR, false>(P, f, d, level, lb.pu, 32, nullptr, lb, acc, tl, lb.pw);
+          work += 32 * (WL + 8);
+          const int rest = fill - 32;
+          int a = 0, b = 0;
+          if (lane < rest) {
+            a = lb.pu[32 + lane];
+            b = lb.pw[32 + lane];
+          }
+          __syncwarp();
+          if (lane < rest) {
+            lb.pu[lane] = a;
+            lb.pw[lane] = b;
+          }
+          fill = rest;
+          __syncwarp();
+        }
+      }
+    }
+    if (act) tl.batches += node_batches(P, (unsigned)ncand_u, wr_u, wl_u, false);
+    work += __reduce_add_sync(FULL, ncand_u);
+  }
+  if (fill) {
+    leaf_parents<INSTR, false>(P, f, d, level, lb.pu, fill, nullptr, lb, acc, tl, lb.pw);
+    work += fill * (WL + 8);
+  }
+  return work;
 }
 
 // Expand node at `level` (1-based): children at level+1 (engine.py:315-374).
@@ -851,6 +983,15 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
       work += expand<INSTR, LAZY>(P, f, d, level, map, lb, acc, tl, ph_);
       if (work > limit) return false;
       fresh = false;
+      const int li0 = level - 1;
+      if (!LAZY && level + 2 == p_eff - 2 && WR <= RP_WORDS && f.ns[li0] > 0 &&
+          !(sink && level + 1 == sink->level)) {
+        // the children's children are leaf-parents: expand every child at once
+        work += expand_children<INSTR>(P, f, d, level, lb, acc, tl);
+        if (work > limit) return false;
+        if (lane == 0) f.ns[li0] = 0;
+        __syncwarp();
+      }
     }
     const int li = level - 1;
     if (level + 1 < p_eff - 2 && f.cur[li] < f.ns[li]) {
@@ -1223,7 +1364,8 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
   const int map_w = (P.map_words + 1) / 2;  // u16 entries packed in words
   uint32_t *my = smem + (int64_t)wib * (map_w + LEAF_WORDS + A.budget_words);
   uint16_t *map = P.map_words ? (uint16_t *)my : nullptr;
-  const LeafBuf lb{(int *)(my + map_w), (int *)(my + map_w + 32)};
+  const LeafBuf lb{(int *)(my + map_w), (int *)(my + map_w + 32), (int *)(my + map_w + 64),
+                   (int *)(my + map_w + 128)};
   uint32_t *my_smem = my + map_w + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   if (map)
@@ -1328,7 +1470,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   uint32_t *my = smem + (int64_t)wib * (LEAF_WORDS + A.budget_words);
-  const LeafBuf lb{(int *)my, (int *)(my + 32)};
+  const LeafBuf lb{(int *)my, (int *)(my + 32), (int *)(my + 64), (int *)(my + 128)};
   uint32_t *my_smem = my + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   Acc128 total{0, 0};
