@@ -968,7 +968,7 @@ __device__ __forceinline__ bool emit_node(const Params &P, const SplitSink &S, c
 // DFS from a node at `start` whose sets sit in setR/setL[start-1].  Returns
 // false once the expansion work passes `limit` (triage: the caller discards
 // the partial task and defers it to the split path).
-template <bool INSTR, bool LAZY>
+template <bool INSTR, bool LAZY, bool FLAT = true>
 __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims &d, int start,
                                     const uint16_t *map, const LeafBuf &lb, Acc128 &acc, Tally &tl,
                                     const SplitSink *sink, PhaseClock &ph_,
@@ -984,7 +984,7 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
       if (work > limit) return false;
       fresh = false;
       const int li0 = level - 1;
-      if (!LAZY && level + 2 == p_eff - 2 && WR <= RP_WORDS && f.ns[li0] > 0 &&
+      if (FLAT && !LAZY && level + 2 == p_eff - 2 && WR <= RP_WORDS && f.ns[li0] > 0 &&
           !(sink && level + 1 == sink->level)) {
         // the children's children are leaf-parents: expand every child at once
         work += expand_children<INSTR>(P, f, d, level, lb, acc, tl);
@@ -1441,7 +1441,8 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
       dfs<INSTR, false>(P, f, d, 1, map, lb, acc, tl, &sink, ph_);
     } else if (TRIAGE) {
       const Tally tl0 = tl;
-      if (!dfs<INSTR, LAZY>(P, f, d, 1, map, lb, acc, tl, nullptr, ph_, A.triage_work)) {
+      if (!dfs<INSTR, LAZY, false>(P, f, d, 1, map, lb, acc, tl, nullptr, ph_,
+                                   A.triage_work)) {
         // over the work budget: discard the partial task, the split path takes it
         tl = tl0;
         if (lane == 0) push_heavy(P, A, j, ns1);
