@@ -237,6 +237,8 @@ struct Frame {
   int *l_pre;
   uint32_t *r_last;  // bit i: local C_R1 index i is the last of its HTB word
   uint32_t *l_last;  // same for C_L1
+  uint32_t *s1;      // level-1 R-survivors as a bitset over the local C_L1 indices
+  uint32_t *s1h;     // the same per C_L1 HTB word (bits of l_val that are survivors)
   int *lids, *lslot, *rids;
   uint32_t *rowR, *rowL;
   int *adjw, *dirw;
@@ -259,6 +261,7 @@ __host__ __device__ __forceinline__ int64_t ro_words(int nR, int nL, int wR, int
   const int64_t WR = (nR + 31) / 32, WL = (nL + 31) / 32;
   int64_t w = 3 * (int64_t)wR + 1 + 3 * (int64_t)wL + 1;  // C_R1 / C_L1 HTB words + prefixes
   w += WR + WL;                                            // r_last, l_last
+  if (sp.compact) w += WL + wL;                            // s1, s1h
   if (!sp.compact) w += nL;                                // lids (compact: lid_of)
   if (sp.lslot()) w += nL;                                 // lslot
   if (sp.compact) w += nR;                                 // rids (C_R1 members)
@@ -302,6 +305,8 @@ __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d,
   f.l_pre = (int *)p; p += d.wL + 1;
   f.r_last = p; p += d.WR;
   f.l_last = p; p += d.WL;
+  f.s1 = p; if (sp.compact) p += d.WL;
+  f.s1h = p; if (sp.compact) p += d.wL;
   f.lids = (int *)p; if (!sp.compact) p += d.nL;
   f.lslot = (int *)p; if (sp.lslot()) p += d.nL;
   f.rids = (int *)p; if (sp.compact) p += d.nR;
@@ -531,6 +536,26 @@ __device__ __forceinline__ int compact_bits(const uint32_t *set, int W, int *can
   return n;
 }
 
+// compact_bits of set & filter
+__device__ __forceinline__ int compact_bits_and(const uint32_t *set, const uint32_t *filter, int W,
+                                                int *cand) {
+  const int lane = lane_id();
+  int n = 0;
+  for (int w0 = 0; w0 < W; w0 += 32) {
+    const uint32_t mine = w0 + lane < W ? set[w0 + lane] & filter[w0 + lane] : 0u;
+    unsigned nz = __ballot_sync(FULL, mine != 0);
+    while (nz) {
+      const int x = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t bits = __shfl_sync(FULL, mine, x);
+      if ((bits >> lane) & 1u) cand[n + __popc(bits & lanemask_lt())] = (w0 + x) * 32 + lane;
+      n += __popc(bits);
+    }
+  }
+  __syncwarp();
+  return n;
+}
+
 struct Tally {
   unsigned long long batches = 0, inter = 0, opw = 0, minw = 0;
 };
@@ -692,6 +717,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
             m = v & dv;
             pre = f.l_pre[k];
             if (m) atomicAdd(&lb.ncand[sl], __popc(m));
+            if (!INSTR && f.compact) m &= f.s1h[k];  // non-survivor leaves add 0
           }
         }
         eval_leaves<INSTR>(P, f, d, R, list + base, sl, v, pre, m, lb.wr[sl], rp, acc, tl);
@@ -704,6 +730,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
         uint32_t m = 0;
         if (act && x < WL) m = Ls[x] & rl[x] & (rl2 ? rl2[x] : FULL);
         ncand += __popc(m);
+        if (!INSTR && f.compact) m &= f.s1[x];
         eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, rp, acc,
                            tl);
       }
@@ -748,8 +775,9 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
     const int wl_u = act ? lane_words(Ls, rl, f.l_last, WL) : 0;
     int ncand_u = 0;
     for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
-      const uint32_t m = act && x < WL ? Ls[x] & rl[x] : 0u;
-      ncand_u += __popc(m);
+      const uint32_t mall = act && x < WL ? Ls[x] & rl[x] : 0u;
+      ncand_u += __popc(mall);
+      const uint32_t m = INSTR || !f.compact ? mall : mall & f.s1[x];
       const int cnt = __popc(m);
       int incl = cnt;
 #pragma unroll
@@ -856,18 +884,26 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
   const uint32_t *Ls = f.setL + li * WL;
   const bool leaf = level + 1 == P.p_eff - 1;
   const bool lp = level + 1 == P.p_eff - 2;  // children are leaf-parents
-  const int ncand = compact_bits(Ls, WL, f.cand);
+  int ncand, ncand_eval;
+  if (INSTR || !f.compact) {
+    ncand = ncand_eval = compact_bits(Ls, WL, f.cand);
+  } else {  // batches count every candidate; only survivors are evaluated
+    int c = 0;
+    for (int w = lane; w < WL; w += 32) c += __popc(Ls[w]);
+    ncand = __reduce_add_sync(FULL, c);
+    ncand_eval = compact_bits_and(Ls, f.s1, WL, f.cand);
+  }
   const int wr = level == 1 ? d.wR : words_touched(R, f.r_last, WR);
   const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_last, WL));
   if (lane == 0) tl.batches += node_batches(P, (unsigned)ncand, wr, wl, leaf);
   int ns = 0;
   const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
   int *out = f.surv + li * f.surv_cap;
-  for (int c0 = 0; c0 < ncand; c0 += 32) {
+  for (int c0 = 0; c0 < ncand_eval; c0 += 32) {
     const int i = c0 + lane;
     bool keep = false;
     int u = 0;
-    if (i < ncand) {
+    if (i < ncand_eval) {
       u = f.cand[i];
       const uint32_t *row = rowR_of(f, d, u);
       int cr = 0;
@@ -905,7 +941,7 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
     }
   }
   __syncwarp();
-  int work = ncand;
+  int work = ncand_eval;
   if (lp && ns) {
     PH_MARK(4);
     leaf_parents<INSTR, LAZY>(P, f, d, level, out, ns, map, lb, acc, tl);
@@ -1234,6 +1270,38 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
       const int e = f.l_pre[k + 1] - 1;
       atomicOr(f.l_last + (e >> 5), 1u << (e & 31));
     }
+  __syncwarp();
+  // level-1 R-survivor masks: candidates outside them cannot pass |R & N(x)| >= q.
+  // Used in compact mode (few survivors among many candidates, e.g. hub pairs);
+  // where most candidates survive the extra masks do not pay.
+  for (int x0 = 0; sp.compact && x0 < d.nL; x0 += 32) {
+    const int x = x0 + lane;
+    bool sv = false;
+    if (x < d.nL) {
+      if (sp.compact || sp.lslot()) {
+        sv = f.lslot[x] >= 0;
+      } else {
+        const uint32_t *row = f.rowR + (int64_t)x * d.WR;
+        int c = 0;
+        for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
+        sv = c >= P.q_eff;
+      }
+    }
+    const unsigned m = __ballot_sync(FULL, sv);
+    if (lane == 0) f.s1[x0 >> 5] = m;
+  }
+  __syncwarp();
+  for (int k = lane; sp.compact && k < d.wL; k += 32) {
+    uint32_t v = f.l_val[k], h = 0;
+    int pos = f.l_pre[k];
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1;
+      if ((f.s1[pos >> 5] >> (pos & 31)) & 1u) h |= 1u << b;
+      pos++;
+    }
+    f.s1h[k] = h;
+  }
   __syncwarp();
   const bool build = sp.rowL && P.p_eff >= 4 && !LAZY;
   if (!build && !INSTR) {
