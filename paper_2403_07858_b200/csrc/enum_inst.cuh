@@ -58,6 +58,16 @@ void BC_SFX(sub_launch)(bool instr, unsigned blocks, size_t smem, cudaStream_t s
   BC_CHECK_LAUNCH();
 }
 
+int BC_SFX(filter_blocks_per_sm)(size_t smem) {
+  return occupancy(filter_kernel<BC_COMPACT != 0>, smem);
+}
+
+void BC_SFX(filter_launch)(unsigned blocks, size_t smem, cudaStream_t st, const Params &P,
+                           const EnumArgs &A) {
+  filter_kernel<BC_COMPACT != 0><<<blocks, ENUM_THREADS, smem, st>>>(P, A);
+  BC_CHECK_LAUNCH();
+}
+
 void BC_SFX(phase_cycles)(unsigned long long *h, bool reset) {
 #ifdef BC_PHASE_PROF
   BC_CUDA(cudaMemcpyFromSymbol(h, g_phase, 16 * sizeof(unsigned long long)));

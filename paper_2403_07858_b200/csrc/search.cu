@@ -1060,7 +1060,35 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               gs.alloc((size_t)blocks * wpb * B.gscratch_words, st);
               B.gscratch = gs.p;
             }
+            DBuf<int32_t> medium, medium_ns1;
+            if (!instr) {
+              // filter: tasks without level-1 survivors finish in a small kernel; the
+              // rest (the medium list) go through the triage kernel
+              const size_t fsmem = (size_t)wpb * (budget + map_w) * 4;
+              const int64_t fblocks =
+                  (int64_t)sms * (compact ? filter_blocks_per_sm_c1(fsmem) : filter_blocks_per_sm_c0(fsmem));
+              medium.alloc(n_alive, st);
+              medium_ns1.alloc(n_alive, st);
+              EnumArgs F = B;
+              F.heavy = medium.p;
+              F.heavy_ns1 = medium_ns1.p;
+              if (B.gscratch && fblocks > blocks) F.gscratch = nullptr;  // (sized for `blocks`)
+              BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
+              BC_CUDA(cudaMemsetAsync(ctr.p + CTR_HEAVY, 0, 8, st));
+              dt.mark("pre-filter");
+              if (compact) filter_launch_c1((unsigned)fblocks, fsmem, st, P, F);
+              else filter_launch_c0((unsigned)fblocks, fsmem, st, P, F);
+              dt.mark("filter");
+              unsigned long long hm = 0;
+              copy_d2h(&hm, ctr.p + CTR_HEAVY, sizeof hm, st);
+              BC_CUDA(cudaStreamSynchronize(st));
+              B.queue = medium.p;
+              B.q1 = (int64_t)hm;
+              launches++;
+              if (dt.on) fprintf(stderr, "[bc search] medium %llu\n", hm);
+            }
             BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
+            BC_CUDA(cudaMemsetAsync(ctr.p + CTR_HEAVY, 0, 8, st));
             dt.mark("pre-triage");
             elaunch(ev, (unsigned)blocks, smem, P, B);
             dt.mark("triage");

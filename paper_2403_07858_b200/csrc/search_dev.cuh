@@ -1154,7 +1154,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
 // for every x by the wedge walk, then sets bits for the survivors only (when
 // they fit the cap); full mode probes a row for every x (local_row).
 // Returns the number of survivors (-1 in full mode without lslot: not counted).
-template <bool INSTR>
+template <bool INSTR, bool ROWS = true>
 __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, const Dims &d,
                                              const FrameSpec &sp, int r, int s, int64_t j,
                                              uint16_t *map, PhaseClock &ph_) {
@@ -1205,7 +1205,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     }
     ns1 = base;
     __syncwarp();
-    if (ns1 > 0 && ns1 <= sp.rows(d.nL)) {
+    if (ROWS && ns1 > 0 && ns1 <= sp.rows(d.nL)) {
       const int64_t total = (int64_t)ns1 * d.WR;
       for (int64_t w = lane; w < total; w += 32) f.rowR[w] = 0;
       __syncwarp();
@@ -1583,6 +1583,66 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
   flush_tallies(P, total, tl, 0, spills, INSTR);
 }
 
+// Triage filter (p_eff >= 5, millions of tasks): only the first half of each task's
+// frame -- C_R1, C_L1 and the level-1 R-survivor count.  A task without survivors
+// is finished here (its level-1 expansion is its only batch work, engine.py:306-331);
+// the others go to `heavy` (the medium list) for the triage kernel.  Kept separate
+// so this kernel, which sees every task, stays small in instruction cache.
+#ifndef FILTER_MIN_BLOCKS
+#define FILTER_MIN_BLOCKS 3
+#endif
+template <bool COMPACT>
+__global__ void __launch_bounds__(ENUM_THREADS, FILTER_MIN_BLOCKS) filter_kernel(Params P, EnumArgs A) {
+  extern __shared__ uint32_t smem[];
+  const int lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int map_w = (P.map_words + 1) / 2;
+  uint32_t *my = smem + (int64_t)wib * (map_w + A.budget_words);
+  uint16_t *map = P.map_words ? (uint16_t *)my : nullptr;
+  uint32_t *my_smem = my + map_w;
+  uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
+  if (map)
+    for (int i = lane; i < map_w; i += 32) my[i] = 0xffffffffu;
+  __syncwarp();
+  Tally tl;
+  Acc128 total{0, 0};
+  unsigned long long claims = 0;
+  const int p_eff = P.p_eff;
+  PH_DECL
+  for (;;) {
+    long long qi = 0;
+    if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
+    qi = __shfl_sync(FULL, qi, 0) + A.q0;
+    if (qi >= A.q1) break;
+    claims++;
+    const int j = A.queue[qi];
+    const int64_t t = P.shard + (int64_t)j * P.nshards;
+    const int2 tk = P.tasks[t];
+    const Dims d = dims_of(A.info[j]);
+    const FrameSpec sp{has_rowL(p_eff, P.map_words), COMPACT, false, A.triage};
+    const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, sp);
+    uint32_t *ro_base = ro <= A.budget_words ? my_smem : my_global;
+    if (!ro_base || (ro_base == my_global && ro > A.gscratch_words)) {
+      if (lane == 0) push_heavy(P, A, j, 0);  // frame over the scratch: the next passes
+      __syncwarp();
+      continue;
+    }
+    Frame f;
+    carve_ro(f, ro_base, d, sp);
+    const int ns1 = build_frame_R<false, false>(P, f, d, sp, tk.x, tk.y, j, map, ph_);
+    clear_map(map, f, d);
+    if (ns1 == 0) {
+      if (lane == 0) tl.batches += node_batches(P, (unsigned)d.nL, d.wR, d.wL, p_eff == 3);
+      finish_task(P, Acc128{0, 0}, t, false, total);
+    } else if (lane == 0) {
+      push_heavy(P, A, j, 0);
+    }
+    __syncwarp();
+  }
+  flush_tallies(P, total, tl, claims, 0, false);
+}
+
 // ---- launchers (defined once per COMPACT value in enum_plain.cu / enum_compact.cu)
 struct EnumVariant {
   bool instr, lazy, split, triage;
@@ -1600,6 +1660,12 @@ void sub_launch_c0(bool instr, unsigned blocks, size_t smem, cudaStream_t st, co
 void sub_launch_c1(bool instr, unsigned blocks, size_t smem, cudaStream_t st, const Params &P,
                    const EnumArgs &A, int64_t n_sub);
 void phase_cycles_c0(unsigned long long *h, bool reset);
+int filter_blocks_per_sm_c0(size_t smem);
+int filter_blocks_per_sm_c1(size_t smem);
+void filter_launch_c0(unsigned blocks, size_t smem, cudaStream_t st, const Params &P,
+                      const EnumArgs &A);
+void filter_launch_c1(unsigned blocks, size_t smem, cudaStream_t st, const Params &P,
+                      const EnumArgs &A);
 void phase_cycles_c1(unsigned long long *h, bool reset);
 
 }  // namespace sk
