@@ -22,7 +22,7 @@ for work, path in zip(args[::2], args[1::2]):
     kn, mn, mv, ki = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
     per = {}
     for r in rows[i0 + 1:]:
-        if len(r) <= mv or not ("enum_kernel" in r[kn] or "sub_kernel" in r[kn]):
+        if len(r) <= mv or not any(k in r[kn] for k in ("enum_kernel", "sub_kernel", "filter_kernel")):
             continue
         per.setdefault(r[ki], {})[r[mn]] = float(r[mv].replace(",", ""))
     dram = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in per.values())
