@@ -297,27 +297,61 @@ __global__ void lower_counts(const int64_t *__restrict__ seg_start, const int32_
     }
 }
 
-// und lists: up(u) copied after the lower part; lower entries u -> und(x) appended
-// (unordered) to the lower part of x, sorted afterwards
-__global__ void und_fill(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
-                         int ntiles, const int32_t *__restrict__ up_ids, int64_t n,
-                         const int64_t *__restrict__ und_off, const int64_t *__restrict__ cnt_low,
-                         unsigned long long *__restrict__ cur_low, int32_t *__restrict__ low_buf,
-                         int32_t *__restrict__ und_out) {
+// directed lists from the upper pairs (u, w), u < w: w in dir2(u) iff rank[w] < rank[u],
+// else u in dir2(w) (graph.py:223).  dup[u]: upper entries kept in dir2(u); dlow[w]:
+// entries of dir2(w) that come from other rows.
+__global__ void dir_counts(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
+                           int ntiles, const int32_t *__restrict__ up_ids,
+                           const int64_t *__restrict__ rank, int64_t n, int64_t *__restrict__ dup,
+                           int64_t *__restrict__ dlow) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = gw; u < n; u += nw) {
-    int64_t pos = und_off[u] + cnt_low[u];
+    const int64_t ru = rank[u];
+    int c = 0;
     for (int ti = 0; ti < ntiles; ti++) {
       const int64_t st = seg_start[u * ntiles + ti];
       const int32_t ln = seg_len[u * ntiles + ti];
       for (int32_t i = lane; i < ln; i += 32) {
-        const int32_t x = up_ids[st + i];
-        und_out[pos + i] = x;
-        low_buf[und_off[x] + (int64_t)atomicAdd(cur_low + x, 1ull)] = (int32_t)u;
+        const int32_t w = up_ids[st + i];
+        if (__ldg(rank + w) < ru) c++;
+        else atomicAdd((unsigned long long *)(dlow + w), 1ull);
       }
-      pos += ln;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) dup[u] = c;
+  }
+}
+
+__global__ void dir_fill(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
+                         int ntiles, const int32_t *__restrict__ up_ids,
+                         const int64_t *__restrict__ rank, int64_t n,
+                         const int64_t *__restrict__ dir_off, const int64_t *__restrict__ dlow,
+                         unsigned long long *__restrict__ cur, int32_t *__restrict__ low_buf,
+                         int32_t *__restrict__ dir_idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n; u += nw) {
+    const int64_t ru = rank[u];
+    int64_t pos = dir_off[u] + dlow[u];
+    for (int ti = 0; ti < ntiles; ti++) {
+      const int64_t st = seg_start[u * ntiles + ti];
+      const int32_t ln = seg_len[u * ntiles + ti];
+      for (int32_t b = 0; b < ln; b += 32) {
+        const int32_t i = b + lane;
+        int32_t w = 0;
+        bool mine = false;
+        if (i < ln) {
+          w = up_ids[st + i];
+          mine = __ldg(rank + w) < ru;
+          if (!mine) low_buf[dir_off[w] + (int64_t)atomicAdd(cur + w, 1ull)] = (int32_t)u;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, mine);
+        if (mine) dir_idx[pos + __popc(m & ((1u << lane) - 1u))] = w;
+        pos += __popc(m);
+      }
     }
   }
 }
@@ -329,15 +363,6 @@ __global__ void add_sizes(const int64_t *__restrict__ a, const int64_t *__restri
   if (i < n) {
     out[i] = a[i] + b[i];
     if (off) low_end[i] = off[i] + b[i];
-  }
-}
-
-__global__ void as_segments(const int64_t *__restrict__ off, const int64_t *__restrict__ size,
-                            int64_t n, int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) {
-    seg_start[i] = off[i];
-    seg_len[i] = (int32_t)size[i];
   }
 }
 
@@ -716,49 +741,19 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       if (attempt == 1) throw Error(BC_ECUDA, "2-hop output overflow after exact resize");
       cap = (int64_t)need;
     }
-    // symmetrise: und(u) = lower part (sorted) ++ up(u)
+    // |und(u)| = |up(u)| + |{w < u : u in up(w)}| (the relation is symmetric); the
+    // directed lists are built from the upper pairs after the priority (below)
     {
-      DBuf<int64_t> low, size, off, low_end;
-      DBuf<unsigned long long> cur;
+      DBuf<int64_t> low;
       low.alloc(n, st);
       low.zero();
-      size.alloc(n + 1, st);
-      size.zero();
-      off.alloc(n + 1, st);
-      low_end.alloc(n, st);
-      cur.alloc(n, st);
-      cur.zero();
       lower_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
                                                         n, low.p);
-      add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, low.p, n, size.p, nullptr,
-                                                     nullptr);
-      exclusive_scan(size.p, off.p, n + 1, st);
-      s.und_pairs = d2h_scalar(off.p + n, st);
       add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, low.p, n, s.und_size.p,
-                                                     low_end.p, off.p);
-      DBuf<int32_t> low_buf, und_full;
-      low_buf.alloc(s.und_pairs ? s.und_pairs : 1, st);
-      und_full.alloc(s.und_pairs ? s.und_pairs : 1, st);
-      und_fill<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p, n,
-                                                    off.p, low.p, cur.p, low_buf.p, und_full.p);
+                                                     nullptr, nullptr);
       BC_CHECK_LAUNCH();
-      if (s.und_pairs > 0) {  // the lower parts, ascending (the upper parts already are)
-        size_t tmp = 0;
-        BC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, low_buf.p, und_full.p,
-                                                    s.und_pairs, n, off.p, low_end.p, st));
-        DBuf<char> t;
-        t.alloc(tmp, st);
-        BC_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, low_buf.p, und_full.p, s.und_pairs,
-                                                    n, off.p, low_end.p, st));
-      }
-      seg_start.alloc(n, st);
-      seg_len.alloc(n, st);
-      as_segments<<<blocks_for(n, 256), 256, 0, st>>>(off.p, s.und_size.p, n, seg_start.p,
-                                                      seg_len.p);
-      BC_CHECK_LAUNCH();
-      und_ids = std::move(und_full);
-      ntiles = 1;
-      L += 7;
+      s.und_pairs = 2 * (int64_t)d2h_scalar(used.p, st);
+      L += 2;
     }
   } else {
     s.und_pairs = 0;
@@ -811,23 +806,49 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
   }
 
   tm.mark("priority");
-  // ---- directed 2-hop lists (graph.py:218-224) ----
+  // ---- directed 2-hop lists (graph.py:218-224) from the upper pairs: a pair (u, w),
+  // u < w, goes to dir2(u) if rank[w] < rank[u], else to dir2(w); dir2(v) is its lower
+  // entries (from other rows, sorted here) followed by its upper ones (already ascending)
   {
-    DBuf<int64_t> dsize;
+    DBuf<int64_t> dup, dlow, dsize, low_end;
+    DBuf<unsigned long long> cur;
+    dup.alloc(n + 1, st);
+    dlow.alloc(n + 1, st);
     dsize.alloc(n + 1, st);
+    low_end.alloc(n + 1, st);
+    cur.alloc(n + 1, st);
+    dup.zero();
+    dlow.zero();
     dsize.zero();
+    cur.zero();
     if (n > 0)
-      directed_filter<false><<<warp_blocks(n, sms), 256, 0, st>>>(
-          seg_start.p, seg_len.p, ntiles, und_ids.p, s.rank.p, n, dsize.p, nullptr, nullptr);
+      dir_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+                                                      s.rank.p, n, dup.p, dlow.p);
+    add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(dup.p, dlow.p, n, dsize.p, nullptr, nullptr);
     s.dir_off.alloc(n + 1, st);
     exclusive_scan(dsize.p, s.dir_off.p, n + 1, st);
     s.dir2_pairs = d2h_scalar(s.dir_off.p + n, st);
     s.dir_idx.alloc(s.dir2_pairs, st);
-    if (n > 0)
-      directed_filter<true><<<warp_blocks(n, sms), 256, 0, st>>>(
-          seg_start.p, seg_len.p, ntiles, und_ids.p, s.rank.p, n, nullptr, s.dir_off.p,
-          s.dir_idx.p);
-    L += 3;
+    DBuf<int32_t> low_buf;
+    low_buf.alloc(s.dir2_pairs ? s.dir2_pairs : 1, st);
+    if (n > 0) {
+      add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(dsize.p, dlow.p, n, dsize.p, low_end.p,
+                                                     s.dir_off.p);
+      dir_fill<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+                                                    s.rank.p, n, s.dir_off.p, dlow.p, cur.p,
+                                                    low_buf.p, s.dir_idx.p);
+      BC_CHECK_LAUNCH();
+    }
+    if (s.dir2_pairs > 0) {
+      size_t tmp = 0;
+      BC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, low_buf.p, s.dir_idx.p,
+                                                  s.dir2_pairs, n, s.dir_off.p, low_end.p, st));
+      DBuf<char> t;
+      t.alloc(tmp, st);
+      BC_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, low_buf.p, s.dir_idx.p, s.dir2_pairs,
+                                                  n, s.dir_off.p, low_end.p, st));
+    }
+    L += 6;
   }
   tm.mark("directed");
   // ---- HTB encodings (htb.py:104-115) ----
