@@ -48,7 +48,7 @@ typedef struct bc_config {
   int32_t order_mode;     /* 0 = reference order (rank == vertex_priority, counters
                              match the reference); 1 = fast ((q,p)-core pruning) */
   int32_t device;         /* CUDA device ordinal */
-  int32_t shard_index;    /* multi-GPU root-task sharding: this rank */
+  int32_t shard_index;    /* multi-GPU sharding (roots, degree-balanced): this rank */
   int32_t shard_count;    /* number of ranks (1 = whole job) */
   int32_t flags;          /* BC_FLAG_* */
   const int64_t *rank_override; /* NULL or one distinct value per anchor vertex
@@ -72,6 +72,8 @@ typedef struct bc_config {
 #define BC_FLAG_L1_PROBE 16     /* level 1 by per-task HTB intersections */
 #define BC_FLAG_ROWR_SCATTER 32 /* candidate rows by wedge scatter where a slot map exists */
 #define BC_FLAG_ROWR_PROBE 64   /* candidate rows by per-candidate intersections */
+#define BC_FLAG_TASK_SHARD 128  /* multi-GPU: tasks interleaved (t % shard_count) instead of
+                                   whole roots dealt degree-balanced (the default) */
 
 /* CountReport (engine.py:64-79) plus device measurements. */
 typedef struct bc_report {

@@ -68,10 +68,10 @@ using namespace sk;
 // ---------------------------------------------------------------------------
 __global__ void p1_kernel(Params P, const int64_t *__restrict__ deg_off) {
   Acc128 a{0, 0};
-  const int64_t nloc = P.n_tasks > P.shard ? (P.n_tasks - P.shard + P.nshards - 1) / P.nshards : 0;
+  const int64_t nloc = P.n_local;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nloc;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = P.shard + j * P.nshards;
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int r = P.tasks[t].x;
     const int d = (int)(deg_off[r + 1] - deg_off[r]);
     Acc128 one{0, 0};
@@ -95,11 +95,11 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
   const int lane = lane_id();
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nloc = P.n_tasks > P.shard ? (P.n_tasks - P.shard + P.nshards - 1) / P.nshards : 0;
+  const int64_t nloc = P.n_local;
   Acc128 a{0, 0};
   unsigned long long alive = 0, inter = 0, opw = 0, minw = 0, maxro = 0, maxscr = 0;
   for (int64_t j = gw; j < nloc; j += nw) {
-    const int64_t t = P.shard + j * P.nshards;
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int2 tk = P.tasks[t];
     int cr, wr;
     if (P.lists) {  // C_R1 from the wedge-scatter pass: |C_R1| and its HTB word count
@@ -346,12 +346,13 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
 }
 
 // development check: |N(r) & N(s)| by merge, thread per local task
-__global__ void l1_naive(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+__global__ void l1_naive(const int2 *__restrict__ tasks, const int64_t *ltask, int64_t nloc,
+                         int shard, int nshards,
                          const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
                          const int64_t *__restrict__ cnt, unsigned long long *bad) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= nloc) return;
-  const int2 tk = tasks[shard + j * nshards];
+  const int2 tk = tasks[task_id(ltask, shard, nshards, j)];
   int64_t a = aoff[tk.x], a1 = aoff[tk.x + 1], b = aoff[tk.y], b1 = aoff[tk.y + 1], c = 0;
   while (a < a1 && b < b1) {
     const int x = aidx[a], y = aidx[b];
@@ -367,13 +368,14 @@ __global__ void l1_naive(const int2 *__restrict__ tasks, int64_t nloc, int shard
 }
 
 // per local task: |C_R1| = sum over its root's chunks (pass-1 columns)
-__global__ void l1_task_totals(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+__global__ void l1_task_totals(const int2 *__restrict__ tasks, const int64_t *ltask, int64_t nloc,
+                               int shard, int nshards,
                                const int64_t *__restrict__ troot, const int64_t *__restrict__ ubase,
                                const int32_t *__restrict__ unit_first, const int64_t *__restrict__ doff,
                                const unsigned long long *__restrict__ aux, int64_t *__restrict__ cnt) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= nloc) return;
-  const int64_t t = shard + j * nshards;
+  const int64_t t = task_id(ltask, shard, nshards, j);
   const int r = tasks[t].x;
   const int64_t k = t - troot[r], D = doff[r + 1] - doff[r];
   const int nch = unit_first[r + 1] - unit_first[r];
@@ -383,13 +385,14 @@ __global__ void l1_task_totals(const int2 *__restrict__ tasks, int64_t nloc, int
 }
 
 // per local task: pass-1 counts -> per-chunk write cursors (list offset + earlier chunks)
-__global__ void l1_cursors(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+__global__ void l1_cursors(const int2 *__restrict__ tasks, const int64_t *ltask, int64_t nloc,
+                               int shard, int nshards,
                            const int64_t *__restrict__ troot, const int64_t *__restrict__ ubase,
                            const int32_t *__restrict__ unit_first, const int64_t *__restrict__ doff,
                            const int64_t *__restrict__ roff, unsigned long long *__restrict__ aux) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= nloc) return;
-  const int64_t t = shard + j * nshards;
+  const int64_t t = task_id(ltask, shard, nshards, j);
   const int r = tasks[t].x;
   const int64_t k = t - troot[r], D = doff[r + 1] - doff[r];
   const int nch = unit_first[r + 1] - unit_first[r];
@@ -405,13 +408,14 @@ __global__ void l1_cursors(const int2 *__restrict__ tasks, int64_t nloc, int sha
 // per root: chunks (units) and aux block size (0 for roots without tasks)
 __global__ void l1_root_sizes(const int64_t *__restrict__ aoff, const int64_t *__restrict__ doff,
                               const int64_t *__restrict__ troot, int64_t n, int32_t *__restrict__ nunits,
-                              int64_t *__restrict__ auxw) {
+                              int64_t *__restrict__ auxw, const int32_t *__restrict__ owner,
+                              int shard) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n) return;
   int32_t nu = 0;
   int64_t w = 0;
   const int64_t D = doff[r + 1] - doff[r];
-  if (troot[r] >= 0 && D > 0) {
+  if (troot[r] >= 0 && D > 0 && (!owner || owner[r] == shard)) {
     const int64_t deg = aoff[r + 1] - aoff[r];
     nu = (int32_t)((deg + L1_CH - 1) / L1_CH);
     w = (int64_t)nu * D;
@@ -436,12 +440,13 @@ __global__ void max_dir_len(const int64_t *__restrict__ doff, int64_t n, unsigne
 
 // probe-cost estimate of level 1 (sum over local tasks of the shorter adjacency
 // slice) vs the wedge pool of the roots: decides the level-1 mode
-__global__ void l1_probe_cost(const int2 *__restrict__ tasks, int64_t nloc, int shard, int nshards,
+__global__ void l1_probe_cost(const int2 *__restrict__ tasks, const int64_t *ltask, int64_t nloc,
+                              int shard, int nshards,
                              const int64_t *__restrict__ hoff, unsigned long long *out) {
   unsigned long long c = 0;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nloc;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const int2 tk = tasks[shard + j * nshards];
+    const int2 tk = tasks[task_id(ltask, shard, nshards, j)];
     const int64_t a = hoff[tk.x + 1] - hoff[tk.x], b = hoff[tk.y + 1] - hoff[tk.y];
     c += (unsigned long long)(a < b ? a : b);
   }
@@ -451,14 +456,15 @@ __global__ void l1_probe_cost(const int2 *__restrict__ tasks, int64_t nloc, int 
 
 __global__ void l1_pool(const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
                         const int64_t *__restrict__ boff, const int64_t *__restrict__ troot,
-                        int64_t n, unsigned long long *out) {
+                        int64_t n, unsigned long long *out, const int32_t *__restrict__ owner,
+                        int shard) {
   // warp per root with tasks: sum of its neighbours' degrees
   const int lane = lane_id();
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long c = 0;
   for (int64_t r = gw; r < n; r += nw) {
-    if (troot[r] < 0) continue;
+    if (troot[r] < 0 || (owner && owner[r] != shard)) continue;
     for (int64_t e = aoff[r] + lane; e < aoff[r + 1]; e += 32) {
       const int v = aidx[e];
       c += (unsigned long long)(boff[v + 1] - boff[v]);
@@ -492,6 +498,34 @@ __global__ void rows_cost(const Info *__restrict__ info, int64_t nloc, int strid
     atomicAdd(out, sc);
     atomicAdd(out + 1, pr);
   }
+}
+
+// root sharding: keys |tasks| x (degree + 1) (0 for roots without tasks), snake owners
+__global__ void root_keys(const int64_t *__restrict__ aoff, const int64_t *__restrict__ doff,
+                          const int64_t *__restrict__ troot, int64_t n,
+                          unsigned long long *__restrict__ keys, int32_t *__restrict__ ids) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const unsigned long long d = (unsigned long long)(doff[r + 1] - doff[r]);
+  keys[r] = troot[r] >= 0 ? d * (unsigned long long)(aoff[r + 1] - aoff[r] + 1) : 0ull;
+  ids[r] = (int32_t)r;
+}
+
+__global__ void snake_owner(const int32_t *__restrict__ sorted, int64_t n, int nshards,
+                            int32_t *__restrict__ owner) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t round = i / nshards, pos = i % nshards;
+  owner[sorted[i]] = (int32_t)(round & 1 ? nshards - 1 - pos : pos);
+}
+
+__global__ void local_task_flags(const int2 *__restrict__ tasks, int64_t n_tasks,
+                                 const int32_t *__restrict__ owner, int shard,
+                                 int64_t *__restrict__ tids, uint8_t *__restrict__ flags) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_tasks) return;
+  tids[t] = t;
+  flags[t] = owner[tasks[t].x] == shard;
 }
 
 __global__ void alive_flags(const uint32_t *cost, int64_t n, uint8_t *flags) {
@@ -651,8 +685,46 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   const int shard = cfg.shard_index;
   if (shard < 0 || shard >= nshards) throw Error(BC_EINVAL, "shard_index out of range");
   const int64_t n_tasks = s.emitted;
-  const int64_t nloc = n_tasks > shard ? (n_tasks - shard + nshards - 1) / nshards : 0;
+  int64_t nloc = n_tasks > shard ? (n_tasks - shard + nshards - 1) / nshards : 0;
   int64_t launches = 0;
+  // Multi-GPU sharding: by root, degree-balanced -- roots ordered by
+  // |tasks| x (degree + 1) and dealt in snake order, each shard keeps whole roots, so the
+  // level-1 wedge walk of a root runs on one GPU only -- or, with BC_FLAG_TASK_SHARD,
+  // task-interleaved (t % shards).  Either way the shard counts sum to the total.
+  DBuf<int32_t> owner;
+  DBuf<int64_t> ltask;
+  if (nshards > 1 && !(cfg.flags & BC_FLAG_TASK_SHARD) && s.n > 0 && n_tasks > 0) {
+    const int64_t n = s.n;
+    DBuf<unsigned long long> keys, skeys;
+    DBuf<int32_t> ids, sids;
+    keys.alloc(n, st);
+    skeys.alloc(n, st);
+    ids.alloc(n, st);
+    sids.alloc(n, st);
+    owner.alloc(n, st);
+    root_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.aoff, s.dir_off.p, s.troot.p, n,
+                                                           keys.p, ids.p);
+    sort_pairs_desc(keys.p, skeys.p, ids.p, sids.p, n, st);
+    snake_owner<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sids.p, n, nshards, owner.p);
+    DBuf<int64_t> tids;
+    DBuf<uint8_t> flags;
+    DBuf<int64_t> nsel;
+    tids.alloc(n_tasks, st);
+    flags.alloc(n_tasks, st);
+    ltask.alloc(n_tasks, st);
+    nsel.alloc(1, st);
+    local_task_flags<<<(unsigned)((n_tasks + 255) / 256), 256, 0, st>>>(s.tasks.p, n_tasks,
+                                                                         owner.p, shard, tids.p,
+                                                                         flags.p);
+    size_t tmp = 0;
+    BC_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, tids.p, flags.p, ltask.p, nsel.p, n_tasks, st));
+    DBuf<char> tb;
+    tb.alloc(tmp, st);
+    BC_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, tids.p, flags.p, ltask.p, nsel.p, n_tasks, st));
+    copy_d2h(&nloc, nsel.p, sizeof nloc, st);
+    BC_CUDA(cudaStreamSynchronize(st));
+    launches += 6;
+  }
 
   std::vector<ulonglong2> comb;
   const int64_t first_bad = binomials(s.q_eff, s.max_deg_anchor, comb);
@@ -679,6 +751,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
                s.dense_id.p, s.dense.p, s.dense_mw, s.boff, s.bidx};
   P.tasks = s.tasks.p;
   P.n_tasks = n_tasks;
+  P.n_local = nloc;
+  P.ltask = ltask.p;
   P.shard = shard;
   P.nshards = nshards;
   P.p_eff = s.p_eff;
@@ -727,8 +801,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       DBuf<unsigned long long> c2;
       c2.alloc(2, st);
       c2.zero();
-      l1_probe_cost<<<sms * 8, 256, 0, st>>>(s.tasks.p, nloc, shard, nshards, s.hadj_off.p, c2.p);
-      l1_pool<<<sms * 8, 256, 0, st>>>(s.aoff, s.aidx, s.boff, s.troot.p, s.n, c2.p + 1);
+      l1_probe_cost<<<sms * 8, 256, 0, st>>>(s.tasks.p, ltask.p, nloc, shard, nshards,
+                                             s.hadj_off.p, c2.p);
+      l1_pool<<<sms * 8, 256, 0, st>>>(s.aoff, s.aidx, s.boff, s.troot.p, s.n, c2.p + 1,
+                                       owner.p, shard);
       BC_CHECK_LAUNCH();
       unsigned long long hc[2];
       copy_d2h(hc, c2.p, sizeof hc, st);
@@ -751,8 +827,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       auxw.alloc(n + 1, st);
       nunits.zero();
       auxw.zero();
-      l1_root_sizes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.aoff, s.dir_off.p, s.troot.p, n,
-                                                                 nunits.p, auxw.p);
+      l1_root_sizes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+          s.aoff, s.dir_off.p, s.troot.p, n, nunits.p, auxw.p, owner.p, shard);
       unit_first.alloc(n + 1, st);
       ubase.alloc(n + 1, st);
       scan_excl(nunits.p, unit_first.p, n + 1, st);
@@ -789,8 +865,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       A1.n_units = n_units;
       A1.aux = aux.p;
       A1.map_words = n <= 65536 ? (int)((n + 31) / 32) : 0;
-      A1.shard = shard;
-      A1.nshards = nshards;
+      A1.shard = owner.p ? 0 : shard;  // root sharding: every slot of an owned root is local
+      A1.nshards = owner.p ? 1 : nshards;
       A1.next = nxt.p;
       const int l1w = L1_THREADS / 32;
       const size_t l1smem = (size_t)l1w * (A1.map_words + (A1.map_words + 1) / 2) * 4;
@@ -810,13 +886,14 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       cnt.alloc(nloc + 1, st);
       cnt.zero();
       l1_task_totals<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
-          s.tasks.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p, s.dir_off.p, aux.p,
-          cnt.p);
+          s.tasks.p, ltask.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p,
+          s.dir_off.p, aux.p, cnt.p);
       if (getenv("BC_CHECK_L1")) {
         DBuf<unsigned long long> bad;
         bad.alloc(1, st);
         bad.zero();
-        l1_naive<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(s.tasks.p, nloc, shard, nshards,
+        l1_naive<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(s.tasks.p, ltask.p, nloc, shard,
+                                                                 nshards,
                                                                  s.aoff, s.aidx, cnt.p, bad.p);
         unsigned long long hb = 0;
         copy_d2h(&hb, bad.p, 8, st);
@@ -830,8 +907,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       BC_CUDA(cudaStreamSynchronize(st));
       l1_lists.alloc(n_entries, st);
       l1_cursors<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
-          s.tasks.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p, s.dir_off.p,
-          l1_roff.p, aux.p);
+          s.tasks.p, ltask.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p,
+          s.dir_off.p, l1_roff.p, aux.p);
       A1.lists = l1_lists.p;
       A1.next = nxt.p + 1;
       dt.mark("l1 offsets");
@@ -1011,7 +1088,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             copy_d2h(&frames_total, sum.p, 8, st);
             BC_CUDA(cudaStreamSynchronize(st));
             launches += 2;
-            if (frames_total <= (int64_t(1) << 28)) T = 0;
+            // (or when the queue is long: a shard of C5 is 2.4 M mostly light tasks)
+            if (frames_total <= (int64_t(1) << 28) && n_alive <= (int64_t(1) << 18)) T = 0;
           }
           if (T > 0) {
             const int budget = env_int("BC_TRIAGE_BUDGET", 1024);

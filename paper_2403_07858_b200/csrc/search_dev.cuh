@@ -69,6 +69,7 @@ struct Params {
   Graph2 g;
   const int2 *__restrict__ tasks;
   int64_t n_tasks;
+  int64_t n_local;  // tasks of this shard
   int shard, nshards;
   int p_eff, q_eff;
   int cap;       // batch_buffer_capacity
@@ -83,7 +84,14 @@ struct Params {
   const int64_t *__restrict__ roff;     // wedge-scatter level 1: C_R1 of local task j is
   const int32_t *__restrict__ lists;    //   lists[roff[j], roff[j+1]) (ascending ids), or null
   int rowR_mode;                        // 0 = per-task choice, 1 = scatter, 2 = probe
-};
+  const int64_t *__restrict__ ltask;    // root sharding: global id of local task j (or null:
+};                                      //   task interleave t = shard + j * nshards)
+
+// global task id of this shard's local task j
+__host__ __device__ __forceinline__ int64_t task_id(const int64_t *ltask, int shard, int nshards,
+                                                    int64_t j) {
+  return ltask ? ltask[j] : shard + j * (int64_t)nshards;
+}
 
 enum { CTR_ALIVE = 0, CTR_BATCHES, CTR_STOLEN, CTR_INTER, CTR_OPW, CTR_MINW, CTR_MAXRO,
        CTR_MAXSCR, CTR_SPILL, CTR_NEXT, CTR_SUB_USED, CTR_SUB_N, CTR_SUB_NEXT, CTR_SPLIT,
@@ -1452,7 +1460,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
     if (qi >= A.q1) break;
     claims++;
     const int j = A.queue[qi];
-    const int64_t t = P.shard + (int64_t)j * P.nshards;
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int2 tk = P.tasks[t];
     const Dims d = dims_of(A.info[j]);
     const FrameSpec sp{SPLIT || has_rowL(p_eff, P.map_words), COMPACT, INSTR,
@@ -1557,7 +1565,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
     const int lv = (int)(rec[1] & 0xff);
     const FrameSpec sp{true, COMPACT, INSTR, (int)(rec[1] >> 8)};
     const int64_t foff = (int64_t)rec[2] | ((int64_t)rec[3] << 32);
-    const int64_t t = P.shard + (int64_t)j * P.nshards;
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const Dims d = dims_of(A.info[j]);
     const int64_t sc = scratch_words(d.nR, d.nL, p_eff, sp);
     uint32_t *sc_base = sc <= A.budget_words ? my_smem : my_global;
@@ -1617,7 +1625,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, FILTER_MIN_BLOCKS) filter_kernel
     if (qi >= A.q1) break;
     claims++;
     const int j = A.queue[qi];
-    const int64_t t = P.shard + (int64_t)j * P.nshards;
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int2 tk = P.tasks[t];
     const Dims d = dims_of(A.info[j]);
     const FrameSpec sp{has_rowL(p_eff, P.map_words), COMPACT, false, A.triage};

@@ -47,6 +47,7 @@ class EngineConfig:
     instrument: bool = False  # tally reference-equivalent intersections (B_enum)
     level1: str = "auto"      # "scatter" (root-grouped wedge walk) | "probe" (per-task HTB)
     rows: str = "auto"        # candidate rows: "scatter" | "probe"
+    shard_mode: str = "root"  # multi-GPU: whole roots, degree-balanced | "task" interleave
 
     def validate(self) -> None:
         if self.worker_count < 1:
@@ -61,6 +62,8 @@ class EngineConfig:
             raise ValueError(f"order_mode must be one of {ORDER_MODES}")
         if self.level1 not in KERNEL_CHOICES or self.rows not in KERNEL_CHOICES:
             raise ValueError(f"level1 / rows must be one of {KERNEL_CHOICES}")
+        if self.shard_mode not in ("root", "task"):
+            raise ValueError("shard_mode must be one of ('root', 'task')")
         if self.enumerate_results:
             raise NotImplementedError(
                 "enumerate_results is not provided by the B200 counting path "
@@ -161,6 +164,8 @@ def _make_config(cfg: EngineConfig, anchor: str, rank, roots, shard=(0, 1), flag
     c.flags |= {"auto": 0, "scatter": _abi.BC_FLAG_L1_SCATTER, "probe": _abi.BC_FLAG_L1_PROBE}[cfg.level1]
     c.flags |= {"auto": 0, "scatter": _abi.BC_FLAG_ROWR_SCATTER,
                 "probe": _abi.BC_FLAG_ROWR_PROBE}[cfg.rows]
+    if cfg.shard_mode == "task":
+        c.flags |= _abi.BC_FLAG_TASK_SHARD
     keep = []
     if rank is not None:
         r = np.ascontiguousarray(rank, dtype=np.int64)

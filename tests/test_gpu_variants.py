@@ -109,3 +109,23 @@ def test_fast_order_rejects_reference_only_inputs():
     g = synth.random_bipartite(40, 40, 0.3, 3)
     with pytest.raises(ValueError):
         count_bicliques(g, 3, 3, EngineConfig(order_mode="fast"), roots=[0, 1])
+
+
+@pytest.mark.parametrize("shard_mode", ["root", "task"])
+def test_shard_modes_sum_to_total(shard_mode):
+    """Both multi-GPU shard rules (whole roots dealt degree-balanced; task interleave)
+    partition the tasks: per-shard counts and consumed tasks add up, on every path."""
+    for name, (p, q) in [("C4", (8, 8)), ("C3", (6, 3)), ("C1", (2, 2))]:
+        g = synth.build_config(name)
+        dg = DeviceGraph(g)
+        full, _ = dg.count_raw(p, q)
+        total = int(full.count_lo) | (int(full.count_hi) << 64)
+        for n in (2, 3, 8):
+            parts = consumed = 0
+            for k in range(n):
+                r, _ = dg.count_raw(p, q, EngineConfig(shard_mode=shard_mode), shard=(k, n))
+                parts += int(r.count_lo) | (int(r.count_hi) << 64)
+                consumed += r.tasks_consumed
+            assert parts == total, (name, n, shard_mode)
+            assert consumed == full.tasks_consumed
+        dg.close()
