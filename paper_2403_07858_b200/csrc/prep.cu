@@ -406,39 +406,6 @@ __global__ void adjacent_dupes(const int64_t *sorted, int64_t n, int *flag) {
   if (i > 0 && i < n && sorted[i] == sorted[i - 1]) atomicExch(flag, 1);
 }
 
-// directed_from_undirected (graph.py:218-224): keep rank[w] < rank[u], order kept.
-template <bool WRITE>
-__global__ void directed_filter(const int64_t *__restrict__ seg_start,
-                                const int32_t *__restrict__ seg_len, int ntiles,
-                                const int32_t *__restrict__ und_ids,
-                                const int64_t *__restrict__ rank, int64_t n,
-                                int64_t *__restrict__ dir_size, const int64_t *__restrict__ dir_off,
-                                int32_t *__restrict__ dir_idx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = gw; u < n; u += nw) {
-    const int64_t ru = rank[u];
-    int64_t pos = WRITE ? dir_off[u] : 0;
-    for (int ti = 0; ti < ntiles; ti++) {
-      const int64_t st = seg_start[u * ntiles + ti];
-      const int32_t ln = seg_len[u * ntiles + ti];
-      for (int32_t b = 0; b < ln; b += 32) {
-        bool keep = false;
-        int32_t w = 0;
-        if (b + lane < ln) {
-          w = und_ids[st + b + lane];
-          keep = __ldg(rank + w) < ru;
-        }
-        const unsigned m = __ballot_sync(FULL, keep);
-        if (WRITE && keep) dir_idx[pos + __popc(m & lanemask_lt())] = w;
-        pos += __popc(m);
-      }
-    }
-    if (!WRITE && lane == 0) dir_size[u] = pos;
-  }
-}
-
 // HTB (htb.py:89-115): per set, idx = distinct id>>5, val = OR of 1<<(id&31).
 template <bool WRITE>
 __global__ void htb_build(const int64_t *__restrict__ off, const int32_t *__restrict__ idx,
