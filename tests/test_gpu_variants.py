@@ -129,3 +129,18 @@ def test_shard_modes_sum_to_total(shard_mode):
             assert parts == total, (name, n, shard_mode)
             assert consumed == full.tasks_consumed
         dg.close()
+
+
+def test_u128_counts_and_overflow():
+    """Complete bipartite graphs: counts above 2^64 are exact (u128 accumulation, limb
+    reduction), a count of 2^128 or more is an error, never a wrapped value."""
+    from math import comb
+
+    nu = nv = 200
+    k = np.arange(nu * nv)
+    g = synth.from_edges(nu, nv, k // nv, k % nv)
+    want = comb(nu, 2) * comb(nv, 20)
+    assert want > 2**64
+    assert count_bicliques(g, 2, 20).count == want
+    with pytest.raises(RuntimeError):
+        count_bicliques(g, 2, 40)  # C(200,2) * C(200,40) > 2^128
