@@ -145,6 +145,15 @@ int bc_graph_create_device(const int64_t *u_off, const int32_t *u_idx, int64_t n
 int bc_graph_count(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg, bc_report *out);
 void bc_graph_destroy(bc_graph *g);
 
+/* Enumeration mode (EngineConfig.enumerate_results, engine.py:271-304, 480-483): every
+ * (p,q)-biclique as a leaf record [L: p_eff anchor-layer ids, c = |C_R|, C_R: c ids], one
+ * record per search leaf with c >= q_eff (it stands for combinations(C_R, q_eff)).  The
+ * records are written to `records` when `*words_needed` <= cap_words; otherwise call again
+ * with a buffer of *words_needed int32 words.  order_mode must be 0. */
+int bc_graph_enumerate(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg,
+                       int32_t *records, int64_t cap_words, int64_t *words_needed,
+                       bc_report *out);
+
 /* Prepared structures on device (prepare_structures, engine.py:115-144),
  * exported for bit-exact comparison against the reference's. */
 int bc_prepare(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg, bc_structs **out);

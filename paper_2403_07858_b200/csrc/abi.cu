@@ -366,6 +366,40 @@ int bc_count(const int64_t *u_off, const int32_t *u_idx, int64_t n_u, const int6
   return rc;
 }
 
+int bc_graph_enumerate(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg,
+                       int32_t *records, int64_t cap_words, int64_t *words_needed,
+                       bc_report *out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  if (out) std::memset(out, 0, sizeof *out);
+  try {
+    if (!h || !cfg || !words_needed) throw bc::Error(BC_EINVAL, "null argument");
+    validate_config(*cfg);
+    if (cfg->order_mode != 0)
+      throw bc::Error(BC_EINVAL, "enumeration needs order_mode 'reference'");
+    if (p < 1 || q < 1) throw bc::Error(BC_EINVAL, "p and q must be >= 1");
+    if (cap_words > 0 && !records) throw bc::Error(BC_EINVAL, "null record buffer");
+    BC_CUDA(cudaSetDevice(h->g.device));
+    bc::DevStructs s;
+    bc::prepare(h->g, p, q, *cfg, s);
+    const int64_t max_words = std::max(s.max_adj_slice, s.max_dir_slice);
+    if (cfg->batch_words < max_words)
+      throw bc::Error(BC_EINVAL, "batch_buffer_capacity " + std::to_string(cfg->batch_words) +
+                                     " words is below the largest candidate slice (" +
+                                     std::to_string(max_words) + " words); raise --batch-words");
+    int64_t launches = 0;
+    *words_needed = bc::enumerate_records(s, records, cap_words, launches);
+    if (out) {
+      fill_from_structs(s, *out);
+      out->kernel_launches += launches;
+    }
+  } catch (const bc::Error &err) {
+    cudaStreamSynchronize(h ? h->g.stream : 0);
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
+}
+
 int bc_prepare(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_structs **out) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_err.clear();

@@ -110,6 +110,11 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out);
 
 int num_sms(int device);
 
+// Enumeration mode (emit.cu): leaf records [L (p_eff ids), |C_R|, C_R ids] of every task,
+// copied to host_out when they fit cap_words; returns the words needed.
+int64_t enumerate_records(const DevStructs &s, int32_t *host_out, int64_t cap_words,
+                          int64_t &launches);
+
 // "fast" order mode (order.cu): the (q_eff, p_eff)-core of the work graph (anchor
 // `layer` becomes U), optionally relabelled by degree; frees with free_graph.
 void fast_order(const DevGraph &g, int layer, int p_eff, int q_eff, bool reorder, DevGraph &out,

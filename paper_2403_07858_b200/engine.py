@@ -64,10 +64,6 @@ class EngineConfig:
             raise ValueError(f"level1 / rows must be one of {KERNEL_CHOICES}")
         if self.shard_mode not in ("root", "task"):
             raise ValueError("shard_mode must be one of ('root', 'task')")
-        if self.enumerate_results:
-            raise NotImplementedError(
-                "enumerate_results is not provided by the B200 counting path "
-                "(SURVEY 8(f) row 4); use the count")
 
 
 @dataclass
@@ -371,7 +367,59 @@ def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
     wall = perf_counter() - t0
     del keep
     layer = structures.choice.layer if structures is not None else "UV"[rep.anchor]
-    return _report(rep, cfg, wall, layer)
+    out = _report(rep, cfg, wall, layer)
+    if cfg.enumerate_results:
+        if roots is not None or structures is not None:
+            raise ValueError("enumerate_results does not combine with roots= / structures=")
+        out.bicliques = enumerate_bicliques(graph, pp, qq, cfg, out.count, layer)
+    return out
+
+
+ENUM_GUARD = 10**7
+
+
+def enumerate_bicliques(g, p: int, q: int, cfg: EngineConfig, count: int, layer: str):
+    """Every (p,q)-biclique as (L, R) tuples, sorted (engine.py:301-304, 480-483).
+
+    The search runs on the GPU (``bc_graph_enumerate``: one record per leaf, [L, |C_R|,
+    C_R]); the host only expands each record into combinations(C_R, q_eff), swaps the
+    pair for a V anchor and sorts."""
+    from itertools import combinations
+
+    if count > ENUM_GUARD:
+        raise ValueError(f"refusing enumeration: {count} results exceeds guard {ENUM_GUARD}")
+    L = _abi.load()
+    dg = DeviceGraph(g, cfg.device)
+    try:
+        c, keep = _make_config(cfg, cfg.anchor, None, None)
+        need = C.c_int64(0)
+        cap = 1 << 16
+        while True:
+            buf = np.zeros(cap, dtype=np.int32)
+            rep = _abi.BcReport()
+            _abi.check(L.bc_graph_enumerate(dg._h, int(p), int(q), C.byref(c), buf.ctypes.data,
+                                            cap, C.byref(need), C.byref(rep)))
+            if need.value <= cap:
+                break
+            cap = int(need.value)
+        del keep
+    finally:
+        dg.close()
+    p_eff, q_eff = rep.p_eff, rep.q_eff
+    found = []
+    rec = buf[:need.value].tolist()
+    i = 0
+    while i < len(rec):
+        left = tuple(sorted(rec[i:i + p_eff]))
+        cnt = rec[i + p_eff]
+        right = rec[i + p_eff + 1:i + p_eff + 1 + cnt]
+        i += p_eff + 1 + cnt
+        for r in combinations(right, q_eff):
+            found.append((left, r))
+    if layer == "V":
+        found = [(r, l) for (l, r) in found]
+    found.sort()
+    return found
 
 
 # ---------------------------------------------------------------------------

@@ -74,8 +74,10 @@ def test_invalid_arguments_fail_before_device(lib):
         count_bicliques(g, 3, 2, EngineConfig(anchor="W"))
     with pytest.raises(ValueError):
         count_bicliques(g, 0, 2)
-    with pytest.raises(NotImplementedError):
-        count_bicliques(g, 3, 2, EngineConfig(enumerate_results=True))
+    with pytest.raises(ValueError):
+        count_bicliques(g, 3, 2, EngineConfig(shard_mode="diagonal"))
+    with pytest.raises(ValueError):
+        count_bicliques(g, 3, 2, EngineConfig(order_mode="fastest"))
 
 
 @pytest.mark.parametrize("x", [0, 1, 2**32 - 1, 2**32, 2**64 + 5, 2**128 - 1, 90068795717])

@@ -144,3 +144,32 @@ def test_u128_counts_and_overflow():
     assert count_bicliques(g, 2, 20).count == want
     with pytest.raises(RuntimeError):
         count_bicliques(g, 2, 40)  # C(200,2) * C(200,40) > 2^128
+
+
+def test_enumeration_matches_brute_force():
+    """enumerate_results (reference engine.py:301-304, 480-483): the device search emits
+    every biclique; sorted (L, R) pairs equal an independent brute-force enumeration,
+    for both anchors and p_eff 1..4."""
+    from itertools import combinations
+
+    def brute(g, p, q):
+        uo, ui = g.u_csr.off, g.u_csr.idx
+        rows = [frozenset(ui[uo[i]:uo[i + 1]].tolist()) for i in range(g.u_count)]
+        out = []
+        for L in combinations(range(g.u_count), p):
+            common = frozenset.intersection(*(rows[u] for u in L))
+            for R in combinations(sorted(common), q):
+                out.append((L, R))
+        return sorted(out)
+
+    g = synth.recon_graph()
+    rep = count_bicliques(g, 3, 2, EngineConfig(enumerate_results=True, anchor="U"))
+    assert rep.bicliques == [((0, 1, 2), (1, 2)), ((0, 1, 3), (0, 2))]  # test_engine.py:42-46
+    for seed, (nu, nv) in enumerate([(9, 9), (8, 10), (12, 7)]):
+        g = synth.random_bipartite(nu, nv, 0.4, seed + 5)
+        for p, q in ((1, 2), (2, 2), (3, 2), (2, 3), (4, 2), (2, 4)):
+            want = brute(g, p, q)
+            for anchor in ("U", "V", "auto"):
+                rep = count_bicliques(g, p, q, EngineConfig(enumerate_results=True, anchor=anchor))
+                assert rep.bicliques == want, (seed, p, q, anchor)
+                assert rep.count == len(want)
