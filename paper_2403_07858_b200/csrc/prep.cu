@@ -837,7 +837,8 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     unsigned long long h[DENSE_NT];
     copy_d2h(h, hist.p, sizeof h, st);
     BC_CUDA(cudaStreamSynchronize(st));
-    const int64_t budget = int64_t(64) << 20;  // bytes of dense rows (stays L2-resident)
+    const char *db = getenv("BC_DENSE_MB");  // development A/B
+    const int64_t budget = int64_t(db ? atoi(db) : 64) << 20;  // bytes of dense rows (L2-sized)
     int pick = -1;
     for (int t = 0; t < DENSE_NT; t++) {
       const int64_t T = int64_t(16) << t;
