@@ -1628,7 +1628,8 @@ __global__ void __launch_bounds__(ENUM_THREADS, FILTER_MIN_BLOCKS) filter_kernel
     const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int2 tk = P.tasks[t];
     const Dims d = dims_of(A.info[j]);
-    const FrameSpec sp{has_rowL(p_eff, P.map_words), COMPACT, false, A.triage};
+    // only C_R1 / C_L1 and the survivor count: no candidate rows
+    const FrameSpec sp{false, COMPACT, false, 1};
     const int64_t ro = ro_words(d.nR, d.nL, d.wR, d.wL, sp);
     uint32_t *ro_base = ro <= A.budget_words ? my_smem : my_global;
     if (!ro_base || (ro_base == my_global && ro > A.gscratch_words)) {
