@@ -154,6 +154,17 @@ int bc_graph_enumerate(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg,
                        int32_t *records, int64_t cap_words, int64_t *words_needed,
                        bc_report *out);
 
+/* Border column reordering (reorder.py:146-179 border_reorder): greedy 1-block
+ * reduction of `layer` (0 = U, 1 = V) by column swaps, on the device.  Writes the
+ * permutation (perm[old id] = new id, n_layer entries) and the 1-block history
+ * (at most iterations + 1 entries, count in *n_history).  Bit-identical to the
+ * reference's choice rules.  iterations < 0 -> BC_EINVAL. */
+int bc_graph_border(bc_graph *g, int32_t layer, int64_t iterations, int64_t *perm,
+                    int64_t *history, int64_t *n_history);
+
+/* Kernel launches of the last bc_graph_border call on this thread. */
+int64_t bc_last_launch_count(void);
+
 /* Prepared structures on device (prepare_structures, engine.py:115-144),
  * exported for bit-exact comparison against the reference's. */
 int bc_prepare(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg, bc_structs **out);

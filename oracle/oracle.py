@@ -58,8 +58,9 @@ class OrcReport(C.Structure):
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(HERE, "bicount_oracle.c")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+    srcs = [os.path.join(HERE, f) for f in ("bicount_oracle.c", "border_oracle.c", "Makefile")]
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
+            os.path.getmtime(s) for s in srcs):
         subprocess.run(["make", "-s", "-C", HERE, "liborc.so"], check=True)
     return LIB_PATH
 
@@ -83,6 +84,9 @@ def lib():
         L.orc_count.restype = C.c_int
         L.orc_count.argtypes = [C.c_void_p, C.POINTER(OrcConfig), C.POINTER(OrcReport)]
         L.orc_last_error.restype = C.c_char_p
+        L.orc_border.restype = C.c_int64
+        L.orc_border.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -314,3 +318,29 @@ def closed_form_count(g, p: int, q: int):
                 shared[a, b] = shared.get((a, b), 0) + 1
         return sum(comb(c, 2) for c in shared.values())
     return None
+
+
+def border_reorder(g, layer: str, iterations: int):
+    """Restates reference ``border_reorder`` (``reorder.py:146-179``) in C
+    (``border_oracle.c``): returns (permutation int64[n], one_block_history list)."""
+    if iterations < 0:
+        raise ValueError("iterations must be >= 0")
+    uo, ui, vo, vi = (np.ascontiguousarray(a) for a in _csr(g))
+    if layer == "U":
+        coff, cidx, roff, ridx = uo, ui, vo, vi
+    elif layer == "V":
+        coff, cidx, roff, ridx = vo, vi, uo, ui
+    else:
+        raise ValueError(f"layer must be 'U' or 'V', got {layer!r}")
+    coff = np.ascontiguousarray(coff, np.int64)
+    roff = np.ascontiguousarray(roff, np.int64)
+    cidx = np.ascontiguousarray(cidx, np.int32)
+    ridx = np.ascontiguousarray(ridx, np.int32)
+    n, m = len(coff) - 1, len(roff) - 1
+    perm = np.empty(max(n, 1), np.int64)
+    hist = np.empty(iterations + 1, np.int64)
+    nh = lib().orc_border(coff.ctypes.data, cidx.ctypes.data, n, roff.ctypes.data,
+                          ridx.ctypes.data, m, iterations, perm.ctypes.data, hist.ctypes.data)
+    if nh < 0:
+        raise MemoryError("orc_border: allocation failed")
+    return perm[:n].copy(), hist[:nh].tolist()

@@ -25,7 +25,8 @@ BC_FLAG_TASK_SHARD = 128
 # every symbol include/bicount_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("bc_abi_version", "bc_last_error", "bc_device_count", "bc_count", "bc_graph_create",
             "bc_graph_create_device", "bc_graph_count", "bc_graph_enumerate", "bc_graph_destroy", "bc_prepare", "bc_export_len", "bc_export",
-            "bc_structs_destroy", "bc_shutdown", "bc_debug_phase_cycles")
+            "bc_structs_destroy", "bc_shutdown", "bc_debug_phase_cycles", "bc_graph_border",
+            "bc_last_launch_count")
 
 
 class BcConfig(C.Structure):
@@ -84,6 +85,11 @@ def _declare(L):
         L.bc_graph_enumerate.restype = C.c_int
         L.bc_graph_enumerate.argtypes = [vp, i32, i32, C.POINTER(BcConfig), vp, i64,
                                          C.POINTER(C.c_int64), C.POINTER(BcReport)]
+    if hasattr(L, "bc_graph_border"):
+        L.bc_graph_border.restype = C.c_int
+        L.bc_graph_border.argtypes = [vp, i32, i64, vp, vp, C.POINTER(C.c_int64)]
+        L.bc_last_launch_count.restype = C.c_int64
+        L.bc_last_launch_count.argtypes = []
     L.bc_graph_destroy.restype = None
     L.bc_graph_destroy.argtypes = [vp]
     L.bc_prepare.restype = C.c_int

@@ -20,6 +20,7 @@ thread_local int64_t t_h2d_bytes = 0, t_d2h_bytes = 0;
 namespace {
 
 thread_local std::string g_err;
+thread_local int64_t g_last_launches = 0;  // kernels of the last bc_graph_border call
 std::mutex g_mu;  // serialise calls (one Python thread drives the library)
 
 // Stream-ordered pool reservation.  Every count allocates its scratch (2-hop ids,
@@ -136,6 +137,8 @@ extern "C" {
 int bc_abi_version(void) { return BC_ABI_VERSION; }
 
 const char *bc_last_error(void) { return g_err.c_str(); }
+
+int64_t bc_last_launch_count(void) { return g_last_launches; }
 
 int bc_device_count(void) {
   int n = 0;
@@ -393,6 +396,26 @@ int bc_graph_enumerate(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg,
       fill_from_structs(s, *out);
       out->kernel_launches += launches;
     }
+  } catch (const bc::Error &err) {
+    cudaStreamSynchronize(h ? h->g.stream : 0);
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
+}
+
+int bc_graph_border(bc_graph *h, int32_t layer, int64_t iterations, int64_t *perm,
+                    int64_t *history, int64_t *n_history) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  try {
+    if (!h || !history || !n_history) throw bc::Error(BC_EINVAL, "null argument");
+    if (iterations < 0) throw bc::Error(BC_EINVAL, "iterations must be >= 0");
+    if (layer != 0 && layer != 1) throw bc::Error(BC_EINVAL, "layer must be 0 (U) or 1 (V)");
+    if (!perm && (layer == 0 ? h->g.n_u : h->g.n_v) > 0) throw bc::Error(BC_EINVAL, "null perm");
+    BC_CUDA(cudaSetDevice(h->g.device));
+    int64_t launches = 0;
+    *n_history = bc::border_reorder(h->g, layer, iterations, perm, history, launches);
+    g_last_launches = launches;
   } catch (const bc::Error &err) {
     cudaStreamSynchronize(h ? h->g.stream : 0);
     return fail(err.code, err.what());

@@ -112,6 +112,10 @@ int num_sms(int device);
 
 // Enumeration mode (emit.cu): leaf records [L (p_eff ids), |C_R|, C_R ids] of every task,
 // copied to host_out when they fit cap_words; returns the words needed.
+// border.cu: reorder.py:146-179 on the device; returns the history length
+int64_t border_reorder(const DevGraph &g, int layer, int64_t iterations, int64_t *perm_out,
+                       int64_t *hist_out, int64_t &launches);
+
 int64_t enumerate_records(const DevStructs &s, int32_t *host_out, int64_t cap_words,
                           int64_t &launches);
 

@@ -1201,7 +1201,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
             // writes every frame to the frame arena and pushes the split-level nodes,
             // then sub_kernel drains them heaviest first with every warp.
-            const int split_level = s.p_eff <= 6 ? 2 : 3;
+            const int split_level = env_int("BC_SPLIT_LEVEL", s.p_eff <= 6 ? 2 : 3);
             const int budget = env_int("BC_SPLIT_BUDGET", 1024);
             const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
             const EnumVariant ev{instr, false, true, false};
