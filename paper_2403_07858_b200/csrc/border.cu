@@ -16,8 +16,9 @@
 //     re-scanning the table every round (reorder.py:71-79 recounts);
 //   * the swap profit of a partner n is decomposed (algebra below) so a round costs
 //     sum_{r in rows(m)} deg(r) + sum over partners of deg(n) hash probes, spread over
-//     the whole GPU, and a round is ~9 back-to-back launches with no host sync (the
-//     host checks the stop flag and table headroom every 64 rounds).
+//     the whole GPU, and a round is ~11 back-to-back launches with no host sync (the
+//     host checks the stop flag and table headroom after rounds 1, 2, 4, .., 64 and
+//     then every 64).
 //
 // Profit decomposition.  one(w) = [popc(w) == 1].  For the chosen column m at
 // position (bm, jm) and a partner n at (bn, jn), bm != bn:
@@ -412,7 +413,7 @@ int64_t border_reorder(const DevGraph &g, int layer, int64_t iterations, int64_t
   BC_CHECK_LAUNCH();
   if (A.ncols >= 2) {
     for (int64_t it = 0; it < iterations; it++) {
-      if (it % CHECK == 0 && it > 0) {
+      if (it > 0 && (it % CHECK == 0 || (it & (it - 1)) == 0)) {  // 1, 2, 4, .. then every 64
         BorderState h{};
         copy_d2h(&h, st.p, sizeof h, s);
         BC_CUDA(cudaStreamSynchronize(s));
