@@ -299,59 +299,90 @@ __global__ void lower_counts(const int64_t *__restrict__ seg_start, const int32_
 
 // directed lists from the upper pairs (u, w), u < w: w in dir2(u) iff rank[w] < rank[u],
 // else u in dir2(w) (graph.py:223).  dup[u]: upper entries kept in dir2(u); dlow[w]:
-// entries of dir2(w) that come from other rows.
+// entries of dir2(w) that come from other rows.  The upper segments are cut into work
+// items of DIR_CHUNK pairs (a hub's list of ~20K pairs is ~80 items, not one warp's
+// serial walk): item_seg[i] = segment of item i, item_off[s] = first item of segment s.
+constexpr int DIR_CHUNK = 256;
+
+__global__ void dir_items(const int32_t *__restrict__ seg_len, int64_t nseg,
+                          int64_t *__restrict__ nitems) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < nseg) nitems[s] = (seg_len[s] + DIR_CHUNK - 1) / DIR_CHUNK;
+}
+
+__global__ void dir_item_owner(const int64_t *__restrict__ item_off, int64_t nseg,
+                               int32_t *__restrict__ item_seg) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < nseg)
+    for (int64_t i = item_off[s]; i < item_off[s + 1]; i++) item_seg[i] = (int32_t)s;
+}
+
 __global__ void dir_counts(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
                            int ntiles, const int32_t *__restrict__ up_ids,
-                           const int64_t *__restrict__ rank, int64_t n, int64_t *__restrict__ dup,
-                           int64_t *__restrict__ dlow) {
+                           const int64_t *__restrict__ rank, const int64_t *__restrict__ item_off,
+                           const int32_t *__restrict__ item_seg, int64_t nseg,
+                           int64_t *__restrict__ dup, int64_t *__restrict__ dlow,
+                           int64_t *__restrict__ item_mine) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = gw; u < n; u += nw) {
+  const int64_t nitems = item_off[nseg];
+  for (int64_t it = gw; it < nitems; it += nw) {
+    const int64_t sg = item_seg[it];
+    const int64_t u = sg / ntiles;
     const int64_t ru = rank[u];
+    const int64_t b0 = (it - item_off[sg]) * DIR_CHUNK;
+    const int64_t rest = seg_len[sg] - b0;
+    const int32_t ln = (int32_t)(rest < DIR_CHUNK ? rest : DIR_CHUNK);
+    const int64_t st = seg_start[sg] + b0;
     int c = 0;
-    for (int ti = 0; ti < ntiles; ti++) {
-      const int64_t st = seg_start[u * ntiles + ti];
-      const int32_t ln = seg_len[u * ntiles + ti];
-      for (int32_t i = lane; i < ln; i += 32) {
-        const int32_t w = up_ids[st + i];
-        if (__ldg(rank + w) < ru) c++;
-        else atomicAdd((unsigned long long *)(dlow + w), 1ull);
-      }
+    for (int32_t i = lane; i < ln; i += 32) {
+      const int32_t w = up_ids[st + i];
+      if (__ldg(rank + w) < ru) c++;
+      else atomicAdd((unsigned long long *)(dlow + w), 1ull);
     }
     c = __reduce_add_sync(0xffffffffu, c);
-    if (lane == 0) dup[u] = c;
+    if (lane == 0) {
+      item_mine[it] = c;
+      if (c) atomicAdd((unsigned long long *)(dup + u), (unsigned long long)c);
+    }
   }
 }
 
+// item_pre: exclusive scan of item_mine; an item's kept upper entries start at
+// dir_off[u] + dlow[u] + (item_pre[it] - item_pre[first item of u]).
 __global__ void dir_fill(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
                          int ntiles, const int32_t *__restrict__ up_ids,
-                         const int64_t *__restrict__ rank, int64_t n,
-                         const int64_t *__restrict__ dir_off, const int64_t *__restrict__ dlow,
-                         unsigned long long *__restrict__ cur, int32_t *__restrict__ low_buf,
-                         int32_t *__restrict__ dir_idx) {
+                         const int64_t *__restrict__ rank, const int64_t *__restrict__ item_off,
+                         const int32_t *__restrict__ item_seg, const int64_t *__restrict__ item_pre,
+                         int64_t nseg, const int64_t *__restrict__ dir_off,
+                         const int64_t *__restrict__ dlow, unsigned long long *__restrict__ cur,
+                         int32_t *__restrict__ low_buf, int32_t *__restrict__ dir_idx) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = gw; u < n; u += nw) {
+  const int64_t nitems = item_off[nseg];
+  for (int64_t it = gw; it < nitems; it += nw) {
+    const int64_t sg = item_seg[it];
+    const int64_t u = sg / ntiles;
     const int64_t ru = rank[u];
-    int64_t pos = dir_off[u] + dlow[u];
-    for (int ti = 0; ti < ntiles; ti++) {
-      const int64_t st = seg_start[u * ntiles + ti];
-      const int32_t ln = seg_len[u * ntiles + ti];
-      for (int32_t b = 0; b < ln; b += 32) {
-        const int32_t i = b + lane;
-        int32_t w = 0;
-        bool mine = false;
-        if (i < ln) {
-          w = up_ids[st + i];
-          mine = __ldg(rank + w) < ru;
-          if (!mine) low_buf[dir_off[w] + (int64_t)atomicAdd(cur + w, 1ull)] = (int32_t)u;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, mine);
-        if (mine) dir_idx[pos + __popc(m & ((1u << lane) - 1u))] = w;
-        pos += __popc(m);
+    const int64_t b0 = (it - item_off[sg]) * DIR_CHUNK;
+    const int64_t rest = seg_len[sg] - b0;
+    const int32_t ln = (int32_t)(rest < DIR_CHUNK ? rest : DIR_CHUNK);
+    const int64_t st = seg_start[sg] + b0;
+    int64_t pos = dir_off[u] + dlow[u] + item_pre[it] - item_pre[item_off[u * ntiles]];
+    for (int32_t b = 0; b < ln; b += 32) {
+      const int32_t i = b + lane;
+      int32_t w = 0;
+      bool mine = false;
+      if (i < ln) {
+        w = up_ids[st + i];
+        mine = __ldg(rank + w) < ru;
+        if (!mine) low_buf[dir_off[w] + (int64_t)atomicAdd(cur + w, 1ull)] = (int32_t)u;
       }
+      const unsigned m = __ballot_sync(0xffffffffu, mine);
+      if (mine) dir_idx[pos + __popc(m & ((1u << lane) - 1u))] = w;
+      pos += __popc(m);
     }
   }
 }
@@ -441,6 +472,42 @@ __global__ void htb_build(const int64_t *__restrict__ off, const int32_t *__rest
     }
     if (!WRITE && lane == 0) words[u] = pos - (WRITE ? hoff[u] : 0);
   }
+}
+
+// Flat HTB build (no per-row tails: a hub row is spread over many threads like any
+// other): flag[i] = entry i starts a word (first of its row, or a new id >> 5), an
+// exclusive scan gives every word its slot, and each word's first entry ORs its run.
+__global__ void htb_rowmark(const int64_t *__restrict__ off, int64_t n, uint8_t *__restrict__ rs) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n && off[u] < off[u + 1]) rs[off[u]] = 1;
+}
+
+__global__ void htb_flags(const int32_t *__restrict__ idx, int64_t E, const uint8_t *__restrict__ rs,
+                          int32_t *__restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E)
+    flag[i] = rs[i] || (((uint32_t)idx[i] >> 5) != ((uint32_t)idx[i - 1] >> 5)) ? 1 : 0;
+  else if (i == E)
+    flag[i] = 0;
+}
+
+__global__ void htb_rowoff(const int64_t *__restrict__ off, int64_t n, const int32_t *__restrict__ wpos,
+                           int64_t *__restrict__ hoff, int64_t *__restrict__ words) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u <= n) hoff[u] = wpos[off[u]];
+  if (u < n) words[u] = (int64_t)wpos[off[u + 1]] - wpos[off[u]];
+}
+
+__global__ void htb_fill(const int32_t *__restrict__ idx, int64_t E, const int32_t *__restrict__ flag,
+                         const int32_t *__restrict__ wpos, uint32_t *__restrict__ hidx,
+                         uint32_t *__restrict__ hval) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E || !flag[i]) return;
+  const uint32_t word = (uint32_t)idx[i] >> 5;
+  uint32_t v = 1u << (idx[i] & 31);
+  for (int64_t j = i + 1; j < E && !flag[j]; j++) v |= 1u << (idx[j] & 31);
+  hidx[wpos[i]] = word;
+  hval[wpos[i]] = v;
 }
 
 // dense hub rows: histogram of rows with more than 16 << i words
@@ -549,17 +616,34 @@ inline unsigned warp_blocks(int64_t n_items, int sms) {
 }
 
 // HTB of a CSR family into (off, idx, val)
-void build_htb(const int64_t *off, const int32_t *idx, int64_t n, DBuf<int64_t> &hoff,
+void build_htb(const int64_t *off, const int32_t *idx, int64_t n, int64_t E, DBuf<int64_t> &hoff,
                DBuf<uint32_t> &hidx, DBuf<uint32_t> &hval, int64_t &total, int64_t &max_slice,
                int sms, cudaStream_t st, int64_t &launches) {
   DBuf<int64_t> words;
   words.alloc(n + 1, st);
   words.zero();
-  htb_build<false><<<warp_blocks(n, sms), 256, 0, st>>>(off, idx, n, words.p, nullptr, nullptr,
-                                                      nullptr);
-  BC_CHECK_LAUNCH();
-  hoff.alloc(n + 1, st);
-  exclusive_scan(words.p, hoff.p, n + 1, st);
+  DBuf<int32_t> flag, wpos;
+  const bool flat = E < (int64_t(1) << 31) - 1;
+  if (flat) {  // word slots by one scan over the entries
+    DBuf<uint8_t> rs;
+    rs.alloc(E + 1, st);
+    rs.zero();
+    flag.alloc(E + 1, st);
+    wpos.alloc(E + 1, st);
+    htb_rowmark<<<blocks_for(n, 256), 256, 0, st>>>(off, n, rs.p);
+    htb_flags<<<blocks_for(E + 1, 256), 256, 0, st>>>(idx, E, rs.p, flag.p);
+    exclusive_scan(flag.p, wpos.p, E + 1, st);
+    hoff.alloc(n + 1, st);
+    htb_rowoff<<<blocks_for(n + 1, 256), 256, 0, st>>>(off, n, wpos.p, hoff.p, words.p);
+    BC_CHECK_LAUNCH();
+    launches += 4;
+  } else {
+    htb_build<false><<<warp_blocks(n, sms), 256, 0, st>>>(off, idx, n, words.p, nullptr, nullptr,
+                                                        nullptr);
+    BC_CHECK_LAUNCH();
+    hoff.alloc(n + 1, st);
+    exclusive_scan(words.p, hoff.p, n + 1, st);
+  }
   DBuf<unsigned long long> mx;
   mx.alloc(1, st);
   mx.zero();
@@ -569,8 +653,11 @@ void build_htb(const int64_t *off, const int32_t *idx, int64_t n, DBuf<int64_t> 
   max_slice = (int64_t)d2h_scalar(mx.p, st);
   hidx.alloc(total, st);
   hval.alloc(total, st);
-  htb_build<true><<<warp_blocks(n, sms), 256, 0, st>>>(off, idx, n, nullptr, hoff.p, hidx.p,
-                                                     hval.p);
+  if (flat)
+    htb_fill<<<blocks_for(E, 256), 256, 0, st>>>(idx, E, flag.p, wpos.p, hidx.p, hval.p);
+  else
+    htb_build<true><<<warp_blocks(n, sms), 256, 0, st>>>(off, idx, n, nullptr, hoff.p, hidx.p,
+                                                       hval.p);
   BC_CHECK_LAUNCH();
   launches += 4;
 }
@@ -788,9 +875,28 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     dlow.zero();
     dsize.zero();
     cur.zero();
-    if (n > 0)
-      dir_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
-                                                      s.rank.p, n, dup.p, dlow.p);
+    // work items: DIR_CHUNK upper pairs each
+    const int64_t nseg = n * ntiles;
+    const int64_t max_items = nseg + s.und_pairs / 2 / DIR_CHUNK + 1;
+    DBuf<int64_t> item_n, item_off, item_mine, item_pre;
+    DBuf<int32_t> item_seg;
+    item_n.alloc(nseg + 1, st);
+    item_off.alloc(nseg + 1, st);
+    item_seg.alloc(max_items, st);
+    item_mine.alloc(max_items + 1, st);
+    item_pre.alloc(max_items + 1, st);
+    item_n.zero();
+    item_mine.zero();
+    if (n > 0) {
+      dir_items<<<blocks_for(nseg, 256), 256, 0, st>>>(seg_len.p, nseg, item_n.p);
+      exclusive_scan(item_n.p, item_off.p, nseg + 1, st);
+      dir_item_owner<<<blocks_for(nseg, 256), 256, 0, st>>>(item_off.p, nseg, item_seg.p);
+      dir_counts<<<(unsigned)sms * 16, 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+                                                     s.rank.p, item_off.p, item_seg.p, nseg, dup.p,
+                                                     dlow.p, item_mine.p);
+      exclusive_scan(item_mine.p, item_pre.p, max_items + 1, st);
+      L += 5;
+    }
     add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(dup.p, dlow.p, n, dsize.p, nullptr, nullptr);
     s.dir_off.alloc(n + 1, st);
     exclusive_scan(dsize.p, s.dir_off.p, n + 1, st);
@@ -801,9 +907,10 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     if (n > 0) {
       add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(dsize.p, dlow.p, n, dsize.p, low_end.p,
                                                      s.dir_off.p);
-      dir_fill<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
-                                                    s.rank.p, n, s.dir_off.p, dlow.p, cur.p,
-                                                    low_buf.p, s.dir_idx.p);
+      dir_fill<<<(unsigned)sms * 16, 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+                                                   s.rank.p, item_off.p, item_seg.p, item_pre.p,
+                                                   nseg, s.dir_off.p, dlow.p, cur.p, low_buf.p,
+                                                   s.dir_idx.p);
       BC_CHECK_LAUNCH();
     }
     if (s.dir2_pairs > 0) {
@@ -819,9 +926,9 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
   }
   tm.mark("directed");
   // ---- HTB encodings (htb.py:104-115) ----
-  build_htb(s.aoff, s.aidx, n, s.hadj_off, s.hadj_idx, s.hadj_val, s.adj_words, s.max_adj_slice,
+  build_htb(s.aoff, s.aidx, n, g.n_e, s.hadj_off, s.hadj_idx, s.hadj_val, s.adj_words, s.max_adj_slice,
             sms, st, L);
-  build_htb(s.dir_off.p, s.dir_idx.p, n, s.hdir_off, s.hdir_idx, s.hdir_val, s.dir2_words,
+  build_htb(s.dir_off.p, s.dir_idx.p, n, s.dir2_pairs, s.hdir_off, s.hdir_idx, s.hdir_val, s.dir2_words,
             s.max_dir_slice, sms, st, L);
 
   tm.mark("htb");
