@@ -54,7 +54,10 @@ T d2h_scalar(const T *p, cudaStream_t st) {
 // the counters, pass 2 writes the kept ids in ascending order with a block-wide
 // exclusive scan.  Cost per vertex is O(pool + n/1024), not O(n).
 // ---------------------------------------------------------------------------
-constexpr int TH_THREADS = 512;
+#ifndef TH_THREADS_DEF
+#define TH_THREADS_DEF 1024
+#endif
+constexpr int TH_THREADS = TH_THREADS_DEF;
 
 template <bool WIDE>
 __device__ __forceinline__ uint32_t ctr_get(const uint32_t *c, int64_t i) {
@@ -75,8 +78,8 @@ template <bool WIDE, bool SUMMARY>
 __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
     const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
     const int64_t *__restrict__ boff, const int32_t *__restrict__ bidx,
-    const int32_t *__restrict__ vorder, int64_t n, uint32_t k, int64_t tile, int ntiles,
-    int *next, int64_t *__restrict__ und_size, int64_t *__restrict__ seg_start,
+    const int32_t *__restrict__ vorder, int64_t n_claim, int64_t n, uint32_t k, int64_t tile,
+    int ntiles, int *next, int64_t *__restrict__ und_size, int64_t *__restrict__ seg_start,
     int32_t *__restrict__ seg_len, int32_t *__restrict__ out_ids, int64_t out_cap,
     unsigned long long *out_used, int *overflow) {
   typedef cub::BlockScan<int, TH_THREADS> Scan;
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
   for (;;) {
     if (tid == 0) {
       int j = atomicAdd(next, 1);
-      s_u = j < n ? vorder[j] : -1;
+      s_u = j < n_claim ? vorder[j] : -1;
     }
     __syncthreads();
     const int64_t u = s_u;
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
 // number at most min(n - 1, pool(u) / k), pool(u) = sum_{v in N(u)} deg(v)
 __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
                              const int64_t *__restrict__ boff, int64_t n, uint32_t k,
-                             unsigned long long *out) {
+                             unsigned long long *out, int32_t *__restrict__ pool_of) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -272,12 +275,141 @@ __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__
       pool += (unsigned long long)(boff[v + 1] - boff[v]);
     }
     pool = warp_sum(pool);
+    if (lane == 0) pool_of[u] = pool < 0x7fffffffull ? (int32_t)pool : 0x7fffffff;
     const unsigned long long b = pool / k;
     tot += b < (unsigned long long)(n - 1) ? b : (unsigned long long)(n - 1);
     ptot += pool;
   }
   if (lane == 0 && tot) atomicAdd(out, tot);
   if (lane == 0 && ptot) atomicAdd(out + 1, ptot);
+}
+
+// Light anchors (pool <= LIGHT_POOL wedges, most vertices of a power-law graph) skip
+// the block kernel's tile counters and its ~10 block barriers per vertex: one warp
+// gathers the vertex's upper wedge ids (w > u) into shared memory, bitonic-sorts them,
+// and keeps every id whose run is >= k long (sorted: buf[i + k - 1] == buf[i]); the
+// kept ids are already ascending.  Same outputs as the block kernel (one segment).
+#ifndef LIGHT_POOL_DEF
+#define LIGHT_POOL_DEF 1024
+#endif
+#ifndef LIGHT_WARPS_DEF
+#define LIGHT_WARPS_DEF 8
+#endif
+constexpr int LIGHT_POOL = LIGHT_POOL_DEF;
+constexpr int LIGHT_WARPS = LIGHT_WARPS_DEF;
+
+__global__ void __launch_bounds__(LIGHT_WARPS * 32) twohop_light(
+    const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
+    const int64_t *__restrict__ boff, const int32_t *__restrict__ bidx,
+    const int32_t *__restrict__ light, int64_t n_light, uint32_t k, int ntiles,
+    int64_t *__restrict__ und_size, int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len,
+    int32_t *__restrict__ out_ids, int64_t out_cap, unsigned long long *out_used, int *overflow) {
+  extern __shared__ int32_t lbuf[];
+  const int lane = threadIdx.x & 31;
+  int32_t *buf = lbuf + (threadIdx.x >> 5) * LIGHT_POOL;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = gw; j < n_light; j += nw) {
+    const int64_t u = light[j];
+    const int64_t e1 = aoff[u + 1];
+    int cnt = 0;
+    for (int64_t e0 = aoff[u]; e0 < e1; e0 += 32) {
+      int64_t st = 0;
+      int len = 0;
+      if (e0 + lane < e1) {
+        const int32_t c = __ldg(aidx + e0 + lane);
+        int64_t lo = __ldg(boff + c), hi = __ldg(boff + c + 1);
+        const int64_t end = hi;
+        while (lo < hi) {  // first id > u
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(bidx + mid) <= u) lo = mid + 1;
+          else hi = mid;
+        }
+        st = lo;
+        len = (int)(end - lo);
+      }
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int excl = incl - len;
+      const int T = __shfl_sync(FULL, incl, 31);
+      for (int r0 = 0; r0 < T; r0 += 32) {
+        const int pos = r0 + lane;
+        int sl = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int c = sl + step;
+          const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
+          if (c < 32 && e <= pos) sl = c;
+        }
+        const int64_t so = __shfl_sync(FULL, st, sl);
+        const int eo = __shfl_sync(FULL, excl, sl);
+        if (pos < T) buf[cnt + pos] = __ldg(bidx + so + (pos - eo));
+      }
+      cnt += T;
+    }
+    int P = 32;
+    while (P < cnt) P <<= 1;
+    for (int i = cnt + lane; i < P; i += 32) buf[i] = 0x7fffffff;
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < (P >> 1); i += 32) {
+          const int a = 2 * stride * (i / stride) + (i % stride), b = a + stride;
+          const int x = buf[a], y = buf[b];
+          const bool up = (a & size) == 0;
+          if ((x > y) == up) {
+            buf[a] = y;
+            buf[b] = x;
+          }
+        }
+        __syncwarp();
+      }
+    int kept = 0;
+    for (int b0 = 0; b0 < cnt; b0 += 32) {
+      const int i = b0 + lane;
+      const bool keep = i < cnt && (i == 0 || buf[i] != buf[i - 1]) && i + (int)k - 1 < cnt &&
+                        buf[i + k - 1] == buf[i];
+      kept += __popc(__ballot_sync(FULL, keep));
+    }
+    long long base = -1;
+    if (lane == 0 && kept) {
+      const unsigned long long bq = atomicAdd(out_used, (unsigned long long)kept);
+      if ((int64_t)bq + kept > out_cap) atomicExch(overflow, 1);
+      else base = (long long)bq;
+    }
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= 0) {
+      int pos = 0;
+      for (int b0 = 0; b0 < cnt; b0 += 32) {
+        const int i = b0 + lane;
+        const bool keep = i < cnt && (i == 0 || buf[i] != buf[i - 1]) && i + (int)k - 1 < cnt &&
+                          buf[i + k - 1] == buf[i];
+        const unsigned m = __ballot_sync(FULL, keep);
+        if (keep) out_ids[base + pos + __popc(m & lanemask_lt())] = buf[i];
+        pos += __popc(m);
+      }
+    }
+    for (int ti = lane; ti < ntiles; ti += 32) {
+      seg_start[u * ntiles + ti] = ti == 0 ? base : -1;
+      seg_len[u * ntiles + ti] = ti == 0 ? kept : 0;
+    }
+    if (lane == 0) und_size[u] = kept;
+    __syncwarp();
+  }
+}
+
+__global__ void light_flags(const int32_t *__restrict__ vorder, const int32_t *__restrict__ pool_of,
+                            int64_t n, uint8_t *__restrict__ is_light, uint8_t *__restrict__ is_heavy) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) {
+    const bool l = pool_of[vorder[j]] <= LIGHT_POOL;
+    is_light[j] = l;
+    is_heavy[j] = !l;
+  }
 }
 
 // The 2-hop relation is symmetric (|N(u) & N(w)| both ways), so the kernel above
@@ -763,19 +895,53 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     ctrs.alloc(2, st);
     used.alloc(2, st);
     used.zero();
-    twohop_bound<<<warp_blocks(n, sms), 256, 0, st>>>(s.aoff, s.aidx, s.boff, n, k, used.p);
+    DBuf<int32_t> pool_of, light_ids, heavy_ids;
+    pool_of.alloc(n, st);
+    twohop_bound<<<warp_blocks(n, sms), 256, 0, st>>>(s.aoff, s.aidx, s.boff, n, k, used.p,
+                                                      pool_of.p);
     BC_CHECK_LAUNCH();
     L++;
+    // light anchors (small wedge pools) go to the warp-per-vertex kernel, the rest keep
+    // the LPT order of the block kernel
+    const bool use_light = !wide && getenv("BC_TH_NOLIGHT") == nullptr;
+    int64_t n_light = 0, n_heavy = n;
+    DBuf<int64_t> nsel;
+    if (use_light) {
+      DBuf<uint8_t> fl, fh;
+      fl.alloc(n, st);
+      fh.alloc(n, st);
+      light_ids.alloc(n, st);
+      heavy_ids.alloc(n, st);
+      nsel.alloc(2, st);
+      light_flags<<<blocks_for(n, 256), 256, 0, st>>>(vorder.p, pool_of.p, n, fl.p, fh.p);
+      size_t stmp = 0;
+      BC_CUDA(cub::DeviceSelect::Flagged(nullptr, stmp, vorder.p, fl.p, light_ids.p, nsel.p, n, st));
+      DBuf<char> t;
+      t.alloc(stmp, st);
+      BC_CUDA(cub::DeviceSelect::Flagged(t.p, stmp, vorder.p, fl.p, light_ids.p, nsel.p, n, st));
+      BC_CUDA(cub::DeviceSelect::Flagged(t.p, stmp, vorder.p, fh.p, heavy_ids.p, nsel.p + 1, n, st));
+      L += 3;
+    }
     unsigned long long hb[2];
     copy_d2h(hb, used.p, sizeof hb, st);
+    if (use_light) {
+      int64_t hn[2];
+      copy_d2h(hn, nsel.p, sizeof hn, st);
+      BC_CUDA(cudaStreamSynchronize(st));
+      n_light = hn[0];
+      n_heavy = hn[1];
+    }
     BC_CUDA(cudaStreamSynchronize(st));
     int64_t cap = std::min<int64_t>((int64_t)hb[0], int64_t(1) << 31);
     cap = std::max<int64_t>(cap, 1);
     // touched-word lists when a vertex's pool is small against the tile's words
-    const bool summary = (double)hb[1] / (double)n < (double)((tile + 31) / 32);
+    bool summary = (double)hb[1] / (double)n < (double)((tile + 31) / 32);
+    if (const char *e = getenv("BC_TH_SUMMARY")) summary = atoi(e) != 0;  // development A/B
     auto kern = wide ? (summary ? twohop_kernel<true, true> : twohop_kernel<true, false>)
                      : (summary ? twohop_kernel<false, true> : twohop_kernel<false, false>);
     BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    BC_CUDA(cudaFuncSetAttribute(twohop_light, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 LIGHT_WARPS * LIGHT_POOL * 4));
     int per_sm = 0;
     BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH_THREADS, smem));
     if (per_sm < 1) per_sm = 1;
@@ -783,12 +949,25 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       und_ids.alloc(cap, st);
       ctrs.zero();
       used.zero();
-      kern<<<sms * per_sm, TH_THREADS, smem, st>>>(s.aoff, s.aidx, s.boff, s.bidx, vorder.p, n, k,
-                                                   tile, ntiles, ctrs.p, s.und_size.p,
-                                                   seg_start.p, seg_len.p, und_ids.p, cap, used.p,
-                                                   ctrs.p + 1);
+      if (n_light > 0) {
+        const size_t lsmem = (size_t)LIGHT_WARPS * LIGHT_POOL * 4;
+        twohop_light<<<(unsigned)std::min<int64_t>((n_light + LIGHT_WARPS - 1) / LIGHT_WARPS,
+                                                   (int64_t)sms * 8),
+                       LIGHT_WARPS * 32, lsmem, st>>>(s.aoff, s.aidx, s.boff, s.bidx, light_ids.p,
+                                                      n_light, k, ntiles, s.und_size.p,
+                                                      seg_start.p, seg_len.p, und_ids.p, cap,
+                                                      used.p, ctrs.p + 1);
+        L++;
+      }
+      if (n_heavy > 0) {
+        kern<<<sms * per_sm, TH_THREADS, smem, st>>>(s.aoff, s.aidx, s.boff, s.bidx,
+                                                     use_light ? heavy_ids.p : vorder.p, n_heavy,
+                                                     n, k, tile, ntiles, ctrs.p, s.und_size.p,
+                                                     seg_start.p, seg_len.p, und_ids.p, cap,
+                                                     used.p, ctrs.p + 1);
+        L++;
+      }
       BC_CHECK_LAUNCH();
-      L++;
       int ovf = d2h_scalar(ctrs.p + 1, st);
       unsigned long long need = d2h_scalar(used.p, st);
       if (!ovf) break;
