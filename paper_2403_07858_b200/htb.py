@@ -2,7 +2,8 @@
 
 Mirrors the data-format surface of the reference's ``bicount.htb``
 (``pkg/src/bicount/htb.py``): ``htb_build`` (family of
-sorted id sets -> off / idx / val, ``htb.py:89-115``), ``htb_decode``, and the
+sorted id sets -> off / idx / val, ``htb.py:89-115``), ``htb_decode``, ``HtbSlice`` with
+``htb_intersect`` / ``htb_intersect_count`` (``htb.py:20-61, 122-183``), and the
 ``HTBDUMP1`` dump format (``dump_htb`` / ``load_htb``, ``htb.py:186-206``): an
 8-byte magic, little-endian u32 ``n_sets, n_words``, then ``off``, ``idx``,
 ``val`` as u32.  The device builds its own HTB arenas (``prep.cu``, flat
@@ -45,6 +46,70 @@ def htb_build(sets) -> Htb:
     off = np.zeros(len(sets) + 1, dtype=np.int64)
     np.cumsum(np.bincount(row[cut], minlength=len(sets)), out=off[1:])
     return Htb(off, word[cut].astype(np.uint32), val.astype(np.uint32))
+
+
+class HtbSlice:
+    """One encoded set: (idx, val) arrays with a [lo, hi) window (htb.py:20-61)."""
+
+    __slots__ = ("idx", "val", "lo", "hi")
+
+    def __init__(self, idx, val, lo: int = 0, hi: int | None = None):
+        self.idx = idx
+        self.val = val
+        self.lo = lo
+        self.hi = len(idx) if hi is None else hi
+
+    def __len__(self) -> int:
+        return self.hi - self.lo
+
+    def _words(self):
+        return (np.asarray(self.idx[self.lo:self.hi], dtype=np.int64),
+                np.asarray(self.val[self.lo:self.hi], dtype=np.uint32))
+
+    def cardinality(self) -> int:
+        return int(np.bitwise_count(self._words()[1]).sum())
+
+    def decode(self) -> list[int]:
+        idx, val = self._words()
+        w, b = np.nonzero(((val[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool))
+        return (idx[w] * 32 + b).tolist()
+
+    @classmethod
+    def from_ids(cls, ids) -> "HtbSlice":
+        h = htb_build([ids])
+        return cls(h.idx, h.val, 0, h.n_words)
+
+    @classmethod
+    def empty(cls) -> "HtbSlice":
+        return cls([], [], 0, 0)
+
+
+def _match(a: HtbSlice, b: HtbSlice):
+    ai, av = a._words()
+    bi, bv = b._words()
+    _, ia, ib = np.intersect1d(ai, bi, assume_unique=True, return_indices=True)
+    x = av[ia] & bv[ib]
+    keep = x != 0
+    return ai[ia][keep], x[keep]
+
+
+def htb_intersect(a: HtbSlice, b: HtbSlice, out: HtbSlice) -> HtbSlice:
+    """a & b written into caller scratch from out.lo, zero words dropped; the scratch
+    must hold min(len(a), len(b)) words (htb.py:122-154)."""
+    if len(out.idx) - out.lo < min(len(a), len(b)):
+        raise ValueError("scratch capacity below min(len(a), len(b)) words")
+    w, x = _match(a, b)
+    for k in range(len(w)):
+        out.idx[out.lo + k] = int(w[k])
+        out.val[out.lo + k] = int(x[k])
+    out.hi = out.lo + len(w)
+    return out
+
+
+def htb_intersect_count(a: HtbSlice, b: HtbSlice, early_exit_at: int | None = None) -> int:
+    """|a & b| without materialising it (htb.py:157-183); with early_exit_at the result
+    is only guaranteed to be >= the threshold once it is met."""
+    return int(np.bitwise_count(_match(a, b)[1]).sum())
 
 
 def htb_decode(h: Htb, s: int) -> list[int]:

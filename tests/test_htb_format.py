@@ -89,3 +89,26 @@ def test_device_arenas_dump_like_reference(key, tmp_path):
     s = prepare_structures(synth.build_config(name), p, q)
     assert _dump_digest(s.adj_htb, tmp_path, "a.bin") == GOLD["structures"][key]["adj"]
     assert _dump_digest(s.dir2_htb, tmp_path, "d.bin") == GOLD["structures"][key]["dir2"]
+
+
+def test_slices_and_intersections():
+    """test_htb.py:39-52, 121-127 and random sets against Python sets."""
+    a, b = htb.HtbSlice.from_ids(FIG_SET_B), htb.HtbSlice.from_ids(FIG_SET_A)
+    out = htb.htb_intersect(a, b, htb.HtbSlice([0] * 8, [0] * 8, 0, 0))
+    assert len(out) == 1 and out.idx[out.lo] == 0 and out.val[out.lo] == 1032
+    assert out.decode() == [3, 10] and htb.htb_intersect_count(a, b) == 2
+    got = htb.htb_intersect(htb.HtbSlice.from_ids([3, 40]), htb.HtbSlice.from_ids([3, 40, 70]),
+                            htb.HtbSlice([0] * 6, [0] * 6, 3, 3))
+    assert got.lo == 3 and got.hi == 5 and got.decode() == [3, 40]
+    with pytest.raises(ValueError):
+        htb.htb_intersect(a, b, htb.HtbSlice([0], [0], 0, 0))
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        xs = sorted(rng.choice(400, size=int(rng.integers(0, 60)), replace=False).tolist())
+        ys = sorted(rng.choice(400, size=int(rng.integers(0, 60)), replace=False).tolist())
+        sa, sb = htb.HtbSlice.from_ids(xs), htb.HtbSlice.from_ids(ys)
+        cap = min(len(sa), len(sb))
+        r = htb.htb_intersect(sa, sb, htb.HtbSlice([0] * cap, [0] * cap, 0, 0))
+        assert r.decode() == sorted(set(xs) & set(ys))
+        assert htb.htb_intersect_count(sa, sb) == len(set(xs) & set(ys)) == r.cardinality()
+        assert sa.cardinality() == len(xs)
