@@ -173,3 +173,45 @@ def test_enumeration_matches_brute_force():
                 rep = count_bicliques(g, p, q, EngineConfig(enumerate_results=True, anchor=anchor))
                 assert rep.bicliques == want, (seed, p, q, anchor)
                 assert rep.count == len(want)
+
+
+def test_wide_counters_and_light_boundaries():
+    """2-hop multiplicities past the 16-bit counters (k > 60000: 32-bit tile counters, no
+    light path) and anchors whose wedge pools straddle the light-kernel bound (1024)."""
+    from math import comb
+
+    nu, nv = 3, 60005
+    k = np.arange(nu * nv)
+    g = synth.from_edges(nu, nv, k // nv, k % nv)
+    rep = count_bicliques(g, 2, 60001, EngineConfig(anchor="U"))
+    assert rep.count == comb(3, 2) * comb(nv, 60001)
+    # stars of growing size around shared centres: pools 1000..1100 per anchor
+    rng = np.random.default_rng(2)
+    for deg in (31, 32, 33, 64):
+        eu, ev = [], []
+        for u in range(40):
+            vs = rng.choice(200, size=deg, replace=False)
+            eu += [u] * deg
+            ev += vs.tolist()
+        g = synth.from_edges(40, 200, eu, ev)
+        for p, q in ((2, 3), (3, 2), (3, 3)):
+            want = O.count(g, p, q, anchor="U")
+            got = count_bicliques(g, p, q, EngineConfig(anchor="U"))
+            assert got.count == want.count and got.batches_executed == want.batches_executed
+
+
+def test_degenerate_inputs():
+    """Empty layers, isolated vertices, p or q above every degree: the reference's counts
+    and counters (all zero or filtered) without a device error."""
+    cases = [synth.from_edges(0, 0, [], []), synth.from_edges(5, 0, [], []),
+             synth.from_edges(0, 7, [], []), synth.from_edges(4, 4, [0], [0]),
+             synth.from_edges(6, 5, [0, 1, 2], [0, 0, 0])]
+    for g in cases:
+        for p, q in ((1, 1), (2, 2), (3, 1), (1, 4), (5, 5)):
+            for anchor in ("auto", "U", "V"):
+                want = O.count(g, p, q, anchor=anchor)
+                got = count_bicliques(g, p, q, EngineConfig(anchor=anchor))
+                assert got.count == want.count, (p, q, anchor)
+                assert got.tasks_emitted == want.tasks_emitted
+                assert got.roots_filtered == want.roots_filtered
+                assert got.batches_executed == want.batches_executed
