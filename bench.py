@@ -15,8 +15,9 @@ workload: BASELINE configs[1] = C2, Chung-Lu 100K x 50K, 1M edges, (4,4).
            intersections, tallied on device) / search time, vs measured HBM.
 * cpu_baseline = the CPU oracle port (oracle/, C + pthreads, all host cores).
 
-Multi-GPU (torchrun): tasks t with t % world == rank run on each rank;
-one NCCL all_reduce of four 32-bit limbs sums the exact partial counts.
+Multi-GPU (torchrun): each rank builds the upper 2-hop lists of its share of the anchors,
+the slices are all-gathered over NCCL, and each rank counts its shard of the tasks (whole
+roots, degree-balanced); one NCCL all_reduce of four 32-bit limbs sums the exact partials.
 """
 
 from __future__ import annotations
@@ -252,7 +253,8 @@ def main():
     import torch.distributed as dist
 
     from paper_2403_07858_b200 import _abi
-    from paper_2403_07858_b200.engine import DeviceGraph, EngineConfig, merge_limbs, split_limbs
+    from paper_2403_07858_b200.engine import (DeviceGraph, EngineConfig, gather_upper, merge_limbs,
+                                              split_limbs)
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -282,8 +284,15 @@ def main():
     dg = DeviceGraph.from_device_csr(*dev_csr, local) if dev_csr is not None else DeviceGraph(g, local)
     del dev_csr
     shard = (rank, world)
+
+    def step():
+        # N > 1: the 2-hop construction is sharded too (each rank builds its anchors'
+        # upper lists, all-gather over NCCL), then every rank counts its task shard
+        upper = gather_upper(dg, p, q, cfg, rank, world) if world > 1 else None
+        return dg.count_raw(p, q, cfg, shard=shard, upper=upper)
+
     for _ in range(args.warmup):
-        dg.count_raw(p, q, cfg, shard=shard)
+        step()
     # B_enum for this workload from the device's own reference-equivalent tally
     instr, _ = dg.count_raw(p, q, EngineConfig(device=local, instrument=True,
                                                batch_buffer_capacity=cap), shard=shard)
@@ -302,7 +311,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            rep, _ = dg.count_raw(p, q, cfg, shard=shard)
+            rep, _ = step()
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))

@@ -115,7 +115,10 @@ enum bc_export_what {
   BC_X_HDIR_VAL = 10, /* uint32[]   */
   BC_X_TASKS = 11,    /* int32[2*emitted] (root, second) in emission order (engine.py:147-173) */
   BC_X_META = 12,     /* int64[4]   anchor, p_eff, q_eff, n */
-  BC_X_COUNT = 13
+  BC_X_SLICE_LENS = 13, /* int32[n] upper 2-hop list length per anchor (bc_graph_twohop_slice;
+                           0 for anchors of other shards) */
+  BC_X_SLICE_IDS = 14,  /* int32[]  the owned anchors' upper lists, anchor order */
+  BC_X_COUNT = 15
 };
 
 typedef struct bc_graph bc_graph;       /* device-resident CSR (both views) */
@@ -164,6 +167,28 @@ int bc_graph_border(bc_graph *g, int32_t layer, int64_t iterations, int64_t *per
 
 /* Kernel launches of the last bc_graph_border call on this thread. */
 int64_t bc_last_launch_count(void);
+
+/* Sharded preprocessing (multi-GPU, one process per GPU).  bc_graph_twohop_slice builds
+ * the upper 2-hop lists ({w > u : |N(u) & N(w)| >= q_eff}, graph.py:192-215 restricted to
+ * the upper triangle) of the anchors shard `shard` of `nshards` owns (snake order over the
+ * LPT order; the union over shards is every anchor); export them with BC_X_SLICE_LENS /
+ * BC_X_SLICE_IDS.  After the ranks exchange them (all-gather), bc_graph_count_upper counts
+ * with the whole upper CSR given in device memory (upper_off int64[n+1], upper_ids
+ * int32[n_pairs], borrowed) and skips the 2-hop construction; results are identical to
+ * bc_graph_count.  order_mode must be 0. */
+int bc_graph_twohop_slice(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg, int32_t shard,
+                          int32_t nshards, bc_structs **out);
+int bc_graph_count_upper(bc_graph *g, int32_t p, int32_t q, const bc_config *cfg,
+                         const int64_t *upper_off, const int32_t *upper_ids, int64_t n_pairs,
+                         bc_report *out);
+/* Whole upper CSR from `world` gathered slices, all device pointers: lens_all int32[world*n]
+ * (rank r's BC_X_SLICE_LENS at r*n), ids_all (rank r's BC_X_SLICE_IDS at r*ids_stride);
+ * writes upper_off int64[n+1] and upper_ids (capacity ids_cap), *n_pairs = pair count. */
+int bc_assemble_upper(int32_t device, int32_t world, int64_t n, const int32_t *lens_all,
+                      const int32_t *ids_all, int64_t ids_stride, int64_t *upper_off,
+                      int32_t *upper_ids, int64_t ids_cap, int64_t *n_pairs);
+/* Like bc_export, into device memory (cudaMemcpy device to device). */
+int bc_export_device(const bc_structs *s, int32_t what, void *device_dst);
 
 /* Prepared structures on device (prepare_structures, engine.py:115-144),
  * exported for bit-exact comparison against the reference's. */

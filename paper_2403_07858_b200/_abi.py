@@ -20,13 +20,14 @@ BC_FLAG_TASK_SHARD = 128
 
 (BC_X_UND_SIZE, BC_X_RANK, BC_X_ORDER, BC_X_DIR_OFF, BC_X_DIR_IDX, BC_X_HADJ_OFF,
  BC_X_HADJ_IDX, BC_X_HADJ_VAL, BC_X_HDIR_OFF, BC_X_HDIR_IDX, BC_X_HDIR_VAL, BC_X_TASKS,
- BC_X_META) = range(13)
+ BC_X_META, BC_X_SLICE_LENS, BC_X_SLICE_IDS) = range(15)
 
 # every symbol include/bicount_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("bc_abi_version", "bc_last_error", "bc_device_count", "bc_count", "bc_graph_create",
             "bc_graph_create_device", "bc_graph_count", "bc_graph_enumerate", "bc_graph_destroy", "bc_prepare", "bc_export_len", "bc_export",
             "bc_structs_destroy", "bc_shutdown", "bc_debug_phase_cycles", "bc_graph_border",
-            "bc_last_launch_count")
+            "bc_last_launch_count", "bc_graph_twohop_slice", "bc_graph_count_upper",
+            "bc_export_device", "bc_assemble_upper")
 
 
 class BcConfig(C.Structure):
@@ -85,6 +86,18 @@ def _declare(L):
         L.bc_graph_enumerate.restype = C.c_int
         L.bc_graph_enumerate.argtypes = [vp, i32, i32, C.POINTER(BcConfig), vp, i64,
                                          C.POINTER(C.c_int64), C.POINTER(BcReport)]
+    if hasattr(L, "bc_graph_twohop_slice"):
+        L.bc_graph_twohop_slice.restype = C.c_int
+        L.bc_graph_twohop_slice.argtypes = [vp, i32, i32, C.POINTER(BcConfig), i32, i32,
+                                            C.POINTER(C.c_void_p)]
+        L.bc_graph_count_upper.restype = C.c_int
+        L.bc_graph_count_upper.argtypes = [vp, i32, i32, C.POINTER(BcConfig), vp, vp, i64,
+                                           C.POINTER(BcReport)]
+        L.bc_export_device.restype = C.c_int
+        L.bc_export_device.argtypes = [vp, i32, vp]
+        L.bc_assemble_upper.restype = C.c_int
+        L.bc_assemble_upper.argtypes = [i32, i32, i64, vp, vp, i64, vp, vp, i64,
+                                        C.POINTER(C.c_int64)]
     if hasattr(L, "bc_graph_border"):
         L.bc_graph_border.restype = C.c_int
         L.bc_graph_border.argtypes = [vp, i32, i64, vp, vp, C.POINTER(C.c_int64)]

@@ -272,7 +272,8 @@ struct WorkGraph {
   ~WorkGraph() { bc::free_graph(g); }
 };
 
-static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_report *out) {
+static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_report *out,
+                      const bc::UpperPairs *upper = nullptr) {
   try {
     if (!h || !cfg || !out) throw bc::Error(BC_EINVAL, "null argument");
     validate_config(*cfg);
@@ -302,7 +303,9 @@ static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, b
       c2.anchor = 0;
       gp = &work.g;
     }
-    bc::prepare(*gp, pp, qq, c2, s);
+    if (upper && cfg->order_mode != 0)
+      throw bc::Error(BC_EINVAL, "injected 2-hop lists need order_mode 'reference'");
+    bc::prepare(*gp, pp, qq, c2, s, upper);
     BC_CUDA(cudaEventRecord(b, h->g.stream));
     // _build_shared capacity check (engine.py:382-391)
     const int64_t max_words = s.max_adj_slice > s.max_dir_slice ? s.max_adj_slice : s.max_dir_slice;
@@ -340,6 +343,79 @@ int bc_graph_count(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_r
     out->d2h_bytes = bc::t_d2h_bytes;
   }
   return rc;
+}
+
+int bc_graph_count_upper(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg,
+                         const int64_t *upper_off, const int32_t *upper_ids, int64_t n_pairs,
+                         bc_report *out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  if (out) std::memset(out, 0, sizeof *out);
+  if (!upper_off || (n_pairs > 0 && !upper_ids) || n_pairs < 0)
+    return fail(BC_EINVAL, "null or negative upper 2-hop arguments");
+  bc::t_h2d_bytes = bc::t_d2h_bytes = 0;
+  const bc::UpperPairs up{upper_off, upper_ids, n_pairs};
+  const int rc = count_impl(h, p, q, cfg, out, &up);
+  if (out) {
+    out->h2d_bytes = bc::t_h2d_bytes;
+    out->d2h_bytes = bc::t_d2h_bytes;
+  }
+  return rc;
+}
+
+int bc_assemble_upper(int32_t device, int32_t world, int64_t n, const int32_t *lens_all,
+                      const int32_t *ids_all, int64_t ids_stride, int64_t *upper_off,
+                      int32_t *upper_ids, int64_t ids_cap, int64_t *n_pairs) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  try {
+    if (!lens_all || !upper_off || !n_pairs || world < 1 || n < 0)
+      throw bc::Error(BC_EINVAL, "bad argument");
+    BC_CUDA(cudaSetDevice(device));
+    cudaStream_t st = nullptr;
+    BC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      *n_pairs = bc::assemble_upper(world, n, lens_all, ids_all, ids_stride, upper_off, upper_ids,
+                                    ids_cap, st, bc::num_sms(device));
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    BC_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  } catch (const bc::Error &err) {
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
+}
+
+int bc_graph_twohop_slice(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, int32_t shard,
+                          int32_t nshards, bc_structs **out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  try {
+    if (!h || !cfg || !out) throw bc::Error(BC_EINVAL, "null argument");
+    *out = nullptr;
+    if (nshards < 1 || shard < 0 || shard >= nshards) throw bc::Error(BC_EINVAL, "bad shard");
+    if (cfg->order_mode != 0) throw bc::Error(BC_EINVAL, "2-hop slices need order_mode 'reference'");
+    if (p < 1 || q < 1) throw bc::Error(BC_EINVAL, "p and q must be >= 1");
+    BC_CUDA(cudaSetDevice(h->g.device));
+    auto *r = new bc_structs;
+    r->g = &h->g;
+    const bc::SliceSpec sl{shard, nshards};
+    try {
+      bc::prepare(h->g, p, q, *cfg, r->s, nullptr, &sl);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+  } catch (const bc::Error &err) {
+    cudaStreamSynchronize(h ? h->g.stream : 0);
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
 }
 
 int bc_count(const int64_t *u_off, const int32_t *u_idx, int64_t n_u, const int64_t *v_off,
@@ -463,8 +539,54 @@ int64_t bc_export_len(const bc_structs *r, int32_t what) {
     case BC_X_HDIR_VAL: return s.dir2_words;
     case BC_X_TASKS: return 2 * s.emitted;
     case BC_X_META: return 4;
+    case BC_X_SLICE_LENS: return s.slice_n_ids >= 0 ? n : -1;
+    case BC_X_SLICE_IDS: return s.slice_n_ids;
   }
   return -1;
+}
+
+// source pointer and element size of an export (device memory)
+static const void *export_src(const bc::DevStructs &s, int32_t what, size_t &el) {
+  el = 8;
+  switch (what) {
+    case BC_X_UND_SIZE: return s.und_size.p;
+    case BC_X_RANK: return s.rank.p;
+    case BC_X_ORDER: return s.order.p;
+    case BC_X_DIR_OFF: return s.dir_off.p;
+    case BC_X_DIR_IDX: el = 4; return s.dir_idx.p;
+    case BC_X_HADJ_OFF: return s.hadj_off.p;
+    case BC_X_HADJ_IDX: el = 4; return s.hadj_idx.p;
+    case BC_X_HADJ_VAL: el = 4; return s.hadj_val.p;
+    case BC_X_HDIR_OFF: return s.hdir_off.p;
+    case BC_X_HDIR_IDX: el = 4; return s.hdir_idx.p;
+    case BC_X_HDIR_VAL: el = 4; return s.hdir_val.p;
+    case BC_X_TASKS: el = 4; return s.tasks.p;
+    case BC_X_SLICE_LENS: el = 4; return s.slice_lens.p;
+    case BC_X_SLICE_IDS: el = 4; return s.slice_ids.p;
+  }
+  return nullptr;
+}
+
+int bc_export_device(const bc_structs *r, int32_t what, void *device_dst) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err.clear();
+  try {
+    if (!r) throw bc::Error(BC_EINVAL, "null argument");
+    const int64_t len = bc_export_len(r, what);
+    if (len < 0 || what == BC_X_META) throw bc::Error(BC_EINVAL, "unknown export id");
+    if (len > 0 && !device_dst) throw bc::Error(BC_EINVAL, "null destination");
+    BC_CUDA(cudaSetDevice(r->g->device));
+    size_t el = 8;
+    const void *src = export_src(r->s, what, el);
+    if (len > 0) {
+      BC_CUDA(cudaMemcpyAsync(device_dst, src, (size_t)len * el, cudaMemcpyDeviceToDevice,
+                              r->s.stream));
+      BC_CUDA(cudaStreamSynchronize(r->s.stream));
+    }
+  } catch (const bc::Error &err) {
+    return fail(err.code, err.what());
+  }
+  return BC_OK;
 }
 
 int bc_export(const bc_structs *r, int32_t what, void *dst) {
@@ -491,6 +613,8 @@ int bc_export(const bc_structs *r, int32_t what, void *dst) {
       case BC_X_HDIR_IDX: src = s.hdir_idx.p; el = 4; break;
       case BC_X_HDIR_VAL: src = s.hdir_val.p; el = 4; break;
       case BC_X_TASKS: src = s.tasks.p; el = 4; break;
+      case BC_X_SLICE_LENS: src = s.slice_lens.p; el = 4; break;
+      case BC_X_SLICE_IDS: src = s.slice_ids.p; el = 4; break;
       case BC_X_META: {
         int64_t *d = (int64_t *)dst;
         d[0] = s.anchor; d[1] = s.p_eff; d[2] = s.q_eff; d[3] = s.n;

@@ -100,10 +100,34 @@ struct DevStructs {
   int64_t max_adj_slice = 0, max_dir_slice = 0;
   int64_t launches = 0;
   cudaStream_t stream = nullptr;
+  // 2-hop slice (sharded preprocessing): upper-list lengths of every anchor (0 unless
+  // owned) and the owned anchors' upper ids in vertex order
+  DBuf<int32_t> slice_lens, slice_ids;
+  int64_t slice_n_ids = -1;
 };
 
-// Preprocessing: anchor choice .. task emission (prep.cu).
-void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s);
+// Sharded preprocessing (multi-GPU): each rank builds the upper 2-hop lists of the
+// anchors it owns; after an all-gather, every rank passes the whole upper CSR back in
+// and prepare() skips the 2-hop construction.
+struct UpperPairs {
+  const int64_t *off;  // device int64[n + 1]
+  const int32_t *ids;  // device int32[pairs], each list ascending, ids > its anchor
+  int64_t pairs;
+};
+struct SliceSpec {
+  int shard, nshards;
+};
+
+// Whole upper CSR from gathered slices (device pointers); returns the pair count.
+int64_t assemble_upper(int world, int64_t n, const int32_t *lens_all, const int32_t *ids_all,
+                       int64_t stride, int64_t *off_out, int32_t *ids_out, int64_t ids_cap,
+                       cudaStream_t st, int sms);
+int num_sms(int device);
+
+// Preprocessing: anchor choice .. task emission (prep.cu).  With `slice`, stops after
+// the owned anchors' upper 2-hop lists (s.slice_*); with `upper`, takes them as given.
+void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s,
+             const UpperPairs *upper = nullptr, const SliceSpec *slice = nullptr);
 
 // Enumeration: level-1 pass + hybrid search (search.cu). Fills counters in out.
 void search(const DevStructs &s, const bc_config &cfg, bc_report &out);

@@ -402,13 +402,58 @@ __global__ void __launch_bounds__(LIGHT_WARPS * 32) twohop_light(
   }
 }
 
+// light / heavy split of the LPT order; with nshards > 1 only the anchors this shard owns
+// (snake order over the LPT positions, so every shard gets a like share of hubs)
 __global__ void light_flags(const int32_t *__restrict__ vorder, const int32_t *__restrict__ pool_of,
-                            int64_t n, uint8_t *__restrict__ is_light, uint8_t *__restrict__ is_heavy) {
+                            int64_t n, int use_light, int shard, int nshards,
+                            uint8_t *__restrict__ is_light, uint8_t *__restrict__ is_heavy) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) {
-    const bool l = pool_of[vorder[j]] <= LIGHT_POOL;
-    is_light[j] = l;
-    is_heavy[j] = !l;
+    const int64_t r = j % (2 * nshards);
+    const bool own = (r < nshards ? r : 2 * nshards - 1 - r) == shard;
+    const bool l = use_light && pool_of[vorder[j]] <= LIGHT_POOL;
+    is_light[j] = own && l;
+    is_heavy[j] = own && !l;
+  }
+}
+
+// injected upper lists -> the per-(anchor, tile) segments the consumers read (one tile)
+__global__ void segs_from_off(const int64_t *__restrict__ off, int64_t n, int64_t *__restrict__ seg_start,
+                              int32_t *__restrict__ seg_len, int64_t *__restrict__ und_size) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n) {
+    seg_start[u] = off[u];
+    seg_len[u] = (int32_t)(off[u + 1] - off[u]);
+    und_size[u] = off[u + 1] - off[u];
+  }
+}
+
+// slice export: upper-list length per anchor, then the ids in anchor order
+__global__ void slice_lens_k(const int32_t *__restrict__ seg_len, int64_t n, int ntiles,
+                             int32_t *__restrict__ lens, int64_t *__restrict__ lens64) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n) {
+    int64_t t = 0;
+    for (int ti = 0; ti < ntiles; ti++) t += seg_len[u * ntiles + ti];
+    lens[u] = (int32_t)t;
+    lens64[u] = t;
+  }
+}
+
+__global__ void slice_copy(const int64_t *__restrict__ seg_start, const int32_t *__restrict__ seg_len,
+                           int64_t n, int ntiles, const int32_t *__restrict__ up_ids,
+                           const int64_t *__restrict__ pos, int32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n; u += nw) {
+    int64_t o = pos[u];
+    for (int ti = 0; ti < ntiles; ti++) {
+      const int64_t st = seg_start[u * ntiles + ti];
+      const int32_t ln = seg_len[u * ntiles + ti];
+      for (int32_t i = lane; i < ln; i += 32) out[o + i] = up_ids[st + i];
+      o += ln;
+    }
   }
 }
 
@@ -822,7 +867,61 @@ struct StageTimer {
   }
 };
 
-void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s) {
+// Whole upper CSR from `world` gathered slices (rank r: lens_all[r * n + u], ids at
+// ids_all[r * stride ...] in anchor order); each anchor's list is in exactly one slice.
+__global__ void up_glens(const int32_t *__restrict__ lens_all, int world, int64_t n,
+                         int64_t *__restrict__ glens, int64_t *__restrict__ flat) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n) {
+    int64_t t = 0;
+    for (int r = 0; r < world; r++) {
+      const int32_t l = lens_all[(int64_t)r * n + u];
+      flat[(int64_t)r * n + u] = l;
+      t += l;
+    }
+    glens[u] = t;
+  }
+}
+
+__global__ void up_copy(const int32_t *__restrict__ lens_all, const int32_t *__restrict__ ids_all,
+                        int64_t stride, int world, int64_t n, const int64_t *__restrict__ pos_flat,
+                        const int64_t *__restrict__ off, int32_t *__restrict__ ids_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n; u += nw) {
+    const int64_t len = off[u + 1] - off[u];
+    if (!len) continue;
+    int r = 0;
+    while (r < world - 1 && lens_all[(int64_t)r * n + u] == 0) r++;
+    const int32_t *src = ids_all + (int64_t)r * stride + (pos_flat[(int64_t)r * n + u] - pos_flat[(int64_t)r * n]);
+    for (int64_t i = lane; i < len; i += 32) ids_out[off[u] + i] = src[i];
+  }
+}
+
+int64_t assemble_upper(int world, int64_t n, const int32_t *lens_all, const int32_t *ids_all,
+                       int64_t stride, int64_t *off_out, int32_t *ids_out, int64_t ids_cap,
+                       cudaStream_t st, int sms) {
+  DBuf<int64_t> glens, flat, pos;
+  glens.alloc(n + 1, st);
+  flat.alloc((size_t)world * n + 1, st);
+  pos.alloc((size_t)world * n + 1, st);
+  glens.zero();
+  flat.zero();
+  up_glens<<<blocks_for(n, 256), 256, 0, st>>>(lens_all, world, n, glens.p, flat.p);
+  exclusive_scan(glens.p, off_out, n + 1, st);
+  exclusive_scan(flat.p, pos.p, (int64_t)world * n + 1, st);
+  const int64_t total = d2h_scalar(off_out + n, st);
+  if (total > ids_cap) throw Error(BC_EINVAL, "upper ids buffer too small");
+  up_copy<<<warp_blocks(n, sms), 256, 0, st>>>(lens_all, ids_all, stride, world, n, pos.p, off_out,
+                                                ids_out);
+  BC_CHECK_LAUNCH();
+  BC_CUDA(cudaStreamSynchronize(st));
+  return total;
+}
+
+void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &s,
+             const UpperPairs *upper, const SliceSpec *slice) {
   if (p < 1 || q < 1) throw Error(BC_EINVAL, "p and q must be >= 1");
   cudaStream_t st = g.stream;
   StageTimer tm(st);
@@ -858,7 +957,23 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
   DBuf<int64_t> seg_start;
   DBuf<int32_t> seg_len;
   DBuf<int32_t> und_ids;
-  if (n > 0 && (int64_t)k <= s.max_deg_anchor) {
+  const int32_t *up_ids = nullptr;  // the upper lists (built here, or injected)
+  if (upper && n > 0) {
+    seg_start.alloc(n, st);
+    seg_len.alloc(n, st);
+    segs_from_off<<<blocks_for(n, 256), 256, 0, st>>>(upper->off, n, seg_start.p, seg_len.p,
+                                                       s.und_size.p);
+    up_ids = upper->ids;
+    DBuf<int64_t> low;
+    low.alloc(n, st);
+    low.zero();
+    lower_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, 1, up_ids, n, low.p);
+    add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, low.p, n, s.und_size.p, nullptr,
+                                                   nullptr);
+    BC_CHECK_LAUNCH();
+    s.und_pairs = 2 * upper->pairs;
+    L += 3;
+  } else if (n > 0 && (int64_t)k <= s.max_deg_anchor) {
     int smem_optin = 0;
     BC_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g.device));
     // counters + touched bitmap per tile id: 2 B + 1/8 B (u16) or 4 B + 1/8 B (u32)
@@ -888,6 +1003,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     L += 3;
     seg_start.alloc((size_t)n * ntiles, st);
     seg_len.alloc((size_t)n * ntiles, st);
+    seg_len.zero();  // anchors of other shards keep empty segments
     // output capacity: the pool bound (exact upper bound; int32 offsets cap it at 2^31,
     // an overflow past that is retried at the exact size)
     DBuf<int> ctrs;  // [0] next vertex, [1] overflow
@@ -904,16 +1020,19 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     // light anchors (small wedge pools) go to the warp-per-vertex kernel, the rest keep
     // the LPT order of the block kernel
     const bool use_light = !wide && getenv("BC_TH_NOLIGHT") == nullptr;
+    const bool select = use_light || slice;
     int64_t n_light = 0, n_heavy = n;
     DBuf<int64_t> nsel;
-    if (use_light) {
+    if (select) {
       DBuf<uint8_t> fl, fh;
       fl.alloc(n, st);
       fh.alloc(n, st);
       light_ids.alloc(n, st);
       heavy_ids.alloc(n, st);
       nsel.alloc(2, st);
-      light_flags<<<blocks_for(n, 256), 256, 0, st>>>(vorder.p, pool_of.p, n, fl.p, fh.p);
+      light_flags<<<blocks_for(n, 256), 256, 0, st>>>(vorder.p, pool_of.p, n, use_light ? 1 : 0,
+                                                      slice ? slice->shard : 0,
+                                                      slice ? slice->nshards : 1, fl.p, fh.p);
       size_t stmp = 0;
       BC_CUDA(cub::DeviceSelect::Flagged(nullptr, stmp, vorder.p, fl.p, light_ids.p, nsel.p, n, st));
       DBuf<char> t;
@@ -924,7 +1043,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     }
     unsigned long long hb[2];
     copy_d2h(hb, used.p, sizeof hb, st);
-    if (use_light) {
+    if (select) {
       int64_t hn[2];
       copy_d2h(hn, nsel.p, sizeof hn, st);
       BC_CUDA(cudaStreamSynchronize(st));
@@ -961,7 +1080,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       }
       if (n_heavy > 0) {
         kern<<<sms * per_sm, TH_THREADS, smem, st>>>(s.aoff, s.aidx, s.boff, s.bidx,
-                                                     use_light ? heavy_ids.p : vorder.p, n_heavy,
+                                                     select ? heavy_ids.p : vorder.p, n_heavy,
                                                      n, k, tile, ntiles, ctrs.p, s.und_size.p,
                                                      seg_start.p, seg_len.p, und_ids.p, cap,
                                                      used.p, ctrs.p + 1);
@@ -974,13 +1093,31 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       if (attempt == 1) throw Error(BC_ECUDA, "2-hop output overflow after exact resize");
       cap = (int64_t)need;
     }
+    up_ids = und_ids.p;
+    if (slice) {  // export this shard's upper lists and stop
+      DBuf<int64_t> l64, pos;
+      s.slice_lens.alloc(n, st);
+      l64.alloc(n + 1, st);
+      pos.alloc(n + 1, st);
+      l64.zero();
+      slice_lens_k<<<blocks_for(n, 256), 256, 0, st>>>(seg_len.p, n, ntiles, s.slice_lens.p, l64.p);
+      exclusive_scan(l64.p, pos.p, n + 1, st);
+      s.slice_n_ids = d2h_scalar(pos.p + n, st);
+      s.slice_ids.alloc(s.slice_n_ids ? s.slice_n_ids : 1, st);
+      slice_copy<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, n, ntiles, up_ids,
+                                                       pos.p, s.slice_ids.p);
+      BC_CHECK_LAUNCH();
+      BC_CUDA(cudaStreamSynchronize(st));
+      L += 4;
+      return;
+    }
     // |und(u)| = |up(u)| + |{w < u : u in up(w)}| (the relation is symmetric); the
     // directed lists are built from the upper pairs after the priority (below)
     {
       DBuf<int64_t> low;
       low.alloc(n, st);
       low.zero();
-      lower_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+      lower_counts<<<warp_blocks(n, sms), 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, up_ids,
                                                         n, low.p);
       add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(s.und_size.p, low.p, n, s.und_size.p,
                                                      nullptr, nullptr);
@@ -995,7 +1132,15 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     seg_len.zero();
     seg_start.zero();
     und_ids.alloc(1, st);
+    up_ids = und_ids.p;
     ntiles = 1;
+    if (slice) {
+      s.slice_lens.alloc(n ? n : 1, st);
+      s.slice_lens.zero();
+      s.slice_n_ids = 0;
+      s.slice_ids.alloc(1, st);
+      return;
+    }
   }
 
   tm.mark("2-hop");
@@ -1070,7 +1215,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       dir_items<<<blocks_for(nseg, 256), 256, 0, st>>>(seg_len.p, nseg, item_n.p);
       exclusive_scan(item_n.p, item_off.p, nseg + 1, st);
       dir_item_owner<<<blocks_for(nseg, 256), 256, 0, st>>>(item_off.p, nseg, item_seg.p);
-      dir_counts<<<(unsigned)sms * 16, 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+      dir_counts<<<(unsigned)sms * 16, 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, up_ids,
                                                      s.rank.p, item_off.p, item_seg.p, nseg, dup.p,
                                                      dlow.p, item_mine.p);
       exclusive_scan(item_mine.p, item_pre.p, max_items + 1, st);
@@ -1086,7 +1231,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     if (n > 0) {
       add_sizes<<<blocks_for(n, 256), 256, 0, st>>>(dsize.p, dlow.p, n, dsize.p, low_end.p,
                                                      s.dir_off.p);
-      dir_fill<<<(unsigned)sms * 16, 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, und_ids.p,
+      dir_fill<<<(unsigned)sms * 16, 256, 0, st>>>(seg_start.p, seg_len.p, ntiles, up_ids,
                                                    s.rank.p, item_off.p, item_seg.p, item_pre.p,
                                                    nseg, s.dir_off.p, dlow.p, cur.p, low_buf.p,
                                                    s.dir_idx.p);

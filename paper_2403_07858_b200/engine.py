@@ -216,9 +216,36 @@ class DeviceGraph:
         self.u_count, self.v_count = nu, nv
         return self
 
+    def twohop_slice(self, p: int, q: int, cfg: EngineConfig | None = None, *, anchor=None,
+                     shard=(0, 1)):
+        """This shard's upper 2-hop lists (sharded preprocessing): (lens int32[n] with 0 for
+        anchors of other shards, ids int32[]) as CUDA tensors (bc_graph_twohop_slice)."""
+        import torch
+
+        cfg = cfg if cfg is not None else EngineConfig()
+        cfg.validate()
+        L = _abi.load()
+        c, keep = _make_config(cfg, anchor or cfg.anchor, None, None)
+        h = C.c_void_p()
+        _abi.check(L.bc_graph_twohop_slice(self._h, int(p), int(q), C.byref(c), int(shard[0]),
+                                           int(shard[1]), C.byref(h)))
+        try:
+            dev = torch.device("cuda", cfg.device)
+            out = []
+            for what in (_abi.BC_X_SLICE_LENS, _abi.BC_X_SLICE_IDS):
+                t = torch.empty(max(int(L.bc_export_len(h, what)), 0), dtype=torch.int32, device=dev)
+                _abi.check(L.bc_export_device(h, what, t.data_ptr() if t.numel() else None))
+                out.append(t)
+        finally:
+            L.bc_structs_destroy(h)
+        del keep
+        return out[0], out[1]
+
     def count_raw(self, p: int, q: int, cfg: EngineConfig | None = None, *, anchor=None,
-                  rank=None, roots=None, shard=(0, 1), task_counts: bool = False):
-        """One counting pass; returns (BcReport, per-task counts or None)."""
+                  rank=None, roots=None, shard=(0, 1), task_counts: bool = False, upper=None):
+        """One counting pass; returns (BcReport, per-task counts or None).  ``upper`` =
+        (off int64[n+1], ids int32[]) CUDA tensors: the whole upper 2-hop CSR from the
+        shards' slices (``assemble_upper``), so the 2-hop construction is skipped."""
         cfg = cfg if cfg is not None else EngineConfig()
         cfg.validate()
         if p < 1 or q < 1:
@@ -234,7 +261,13 @@ class DeviceGraph:
             c.task_counts = tc.ctypes.data
             c.task_counts_cap = cap
         rep = _abi.BcReport()
-        _abi.check(L.bc_graph_count(self._h, int(p), int(q), C.byref(c), C.byref(rep)))
+        if upper is None:
+            _abi.check(L.bc_graph_count(self._h, int(p), int(q), C.byref(c), C.byref(rep)))
+        else:
+            off, ids = upper
+            _abi.check(L.bc_graph_count_upper(self._h, int(p), int(q), C.byref(c),
+                                              off.data_ptr(), ids.data_ptr() if ids.numel() else None,
+                                              int(ids.numel()), C.byref(rep)))
         del keep
         per_task = None
         if task_counts:
@@ -452,14 +485,82 @@ def allreduce_count(partial: int, group=None, device=None) -> int:
     return merge_limbs(t.cpu().tolist())
 
 
+def assemble_upper(slices):
+    """Whole upper 2-hop CSR from every shard's (lens, ids) slice (each anchor's list comes
+    from exactly one shard, in anchor order within a slice): (off int64[n+1], ids int32[])."""
+    import torch
+
+    lens = torch.stack([sl[0] for sl in slices]).sum(0).to(torch.int64)
+    n = lens.numel()
+    off = torch.zeros(n + 1, dtype=torch.int64, device=lens.device)
+    torch.cumsum(lens, 0, out=off[1:])
+    ids = torch.empty(int(off[-1].item()), dtype=torch.int32, device=lens.device)
+    for sl_lens, sl_ids in slices:
+        if sl_ids.numel() == 0:
+            continue
+        l64 = sl_lens.to(torch.int64)
+        starts = off[:-1][l64 > 0]
+        cnt = l64[l64 > 0]
+        first = torch.repeat_interleave(starts - (torch.cumsum(cnt, 0) - cnt), cnt)
+        ids[first + torch.arange(sl_ids.numel(), device=lens.device)] = sl_ids
+    return off, ids
+
+
+def assemble_upper_device(lens_all, ids_all, stride: int, n_pairs: int, device: int = 0):
+    """``assemble_upper`` on the device (bc_assemble_upper): lens_all int32[world * n],
+    ids_all int32[world * stride] (rank r's slice ids at r * stride)."""
+    import torch
+
+    L = _abi.load()
+    world = ids_all.numel() // max(stride, 1) if stride else lens_all.numel()
+    n = lens_all.numel() // world
+    off = torch.empty(n + 1, dtype=torch.int64, device=lens_all.device)
+    ids = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=lens_all.device)
+    got = C.c_int64(0)
+    _abi.check(L.bc_assemble_upper(int(device), int(world), int(n), lens_all.data_ptr(),
+                                   ids_all.data_ptr(), int(stride), off.data_ptr(), ids.data_ptr(),
+                                   int(ids.numel()), C.byref(got)))
+    return off, ids[:got.value]
+
+
+def gather_upper(dg: DeviceGraph, p: int, q: int, cfg: EngineConfig, rank: int, world: int,
+                 group=None, anchor=None):
+    """Sharded preprocessing: build this rank's 2-hop slice, all-gather every slice
+    (NCCL over NVLink; variable sizes padded to the largest), assemble the whole upper CSR."""
+    import torch
+    import torch.distributed as dist
+
+    lens, ids = dg.twohop_slice(p, q, cfg, anchor=anchor, shard=(rank, world))
+    dev = lens.device
+    # NCCL gathers device memory directly; gloo (CPU tests) goes through host copies
+    cdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
+    sizes = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([ids.numel()], dtype=torch.int64, device=cdev), group=group)
+    mx = max(int(x.item()) for x in sizes)
+    pad = torch.zeros(max(mx, 1), dtype=torch.int32, device=cdev)
+    pad[:ids.numel()] = ids.to(cdev)
+    all_ids = [torch.empty_like(pad) for _ in range(world)]
+    all_lens = [torch.empty(lens.numel(), dtype=torch.int32, device=cdev) for _ in range(world)]
+    dist.all_gather(all_ids, pad, group=group)
+    dist.all_gather(all_lens, lens.to(cdev), group=group)
+    total = sum(int(x.item()) for x in sizes)
+    return assemble_upper_device(torch.cat(all_lens).to(dev), torch.cat(all_ids).to(dev),
+                                 pad.numel(), total, dev.index or 0)
+
+
 def count_bicliques_distributed(g, p: int, q: int, cfg: EngineConfig | None = None, *,
                                 rank: int, world: int, group=None, dgraph: DeviceGraph | None = None,
-                                roots=None) -> tuple[int, CountReport]:
-    """This rank counts tasks t with t % world == rank; returns (total, local report)."""
+                                roots=None, shard_prep: bool = False) -> tuple[int, CountReport]:
+    """This rank counts its shard of the tasks (cfg.shard_mode); returns (total, local
+    report).  With ``shard_prep`` the 2-hop construction is split across the ranks too
+    (``gather_upper``) instead of being replicated."""
     cfg = cfg if cfg is not None else EngineConfig()
     dg = dgraph if dgraph is not None else DeviceGraph(g, cfg.device)
     t0 = perf_counter()
-    rep, _ = dg.count_raw(p, q, cfg, roots=roots, shard=(rank, world))
+    upper = None
+    if shard_prep and world > 1 and cfg.order_mode == "reference":
+        upper = gather_upper(dg, p, q, cfg, rank, world, group)
+    rep, _ = dg.count_raw(p, q, cfg, roots=roots, shard=(rank, world), upper=upper)
     wall = perf_counter() - t0
     local = _report(rep, cfg, wall, "UV"[rep.anchor])
     import torch

@@ -10,6 +10,7 @@ exact total on every rank, including totals far above 2^64.
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
@@ -74,3 +75,25 @@ def test_c4_shard_partials():
     partials = [sum(r.task_counts[k::2]) for k in range(2)]
     assert r.count == 90068795717
     _run(partials, r.count)
+
+
+def test_assemble_upper_cpu():
+    """Slices of an upper CSR dealt to 3 shards reassemble into the original (CPU tensors)."""
+    import torch
+
+    from paper_2403_07858_b200.engine import assemble_upper
+
+    rng = np.random.default_rng(1)
+    n = 50
+    lists = [np.sort(rng.choice(np.arange(u + 1, n + 40), size=int(rng.integers(0, 6)),
+                                replace=False)) if u < n else [] for u in range(n)]
+    lens = torch.tensor([len(x) for x in lists], dtype=torch.int32)
+    owner = torch.tensor([u % 3 for u in range(n)])
+    slices = []
+    for k in range(3):
+        lk = torch.where(owner == k, lens, torch.zeros_like(lens))
+        ids = [int(v) for u in range(n) if u % 3 == k for v in lists[u]]
+        slices.append((lk, torch.tensor(ids, dtype=torch.int32)))
+    off, ids = assemble_upper(slices)
+    assert off.tolist() == np.concatenate([[0], np.cumsum([len(x) for x in lists])]).tolist()
+    assert ids.tolist() == [int(v) for x in lists for v in x]
