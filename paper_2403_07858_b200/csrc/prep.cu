@@ -780,6 +780,11 @@ __global__ void max_reduce(const int64_t *a, int64_t n, unsigned long long *out)
   if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
 }
 
+inline int64_t env_i64(const char *name, int64_t dflt) {  // development A/B knobs
+  const char *e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+
 inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   return (unsigned)(b < 1 ? 1 : b);
@@ -800,7 +805,9 @@ void build_htb(const int64_t *off, const int32_t *idx, int64_t n, int64_t E, DBu
   words.alloc(n + 1, st);
   words.zero();
   DBuf<int32_t> flag, wpos;
-  const bool flat = E < (int64_t(1) << 31) - 1;
+  // small families keep the per-row kernels (fewer launches); large ones go flat
+  const int64_t flat_min = env_i64("BC_HTB_FLAT_MIN", int64_t(1) << 17);
+  const bool flat = E >= flat_min && E < (int64_t(1) << 31) - 1;
   if (flat) {  // word slots by one scan over the entries
     DBuf<uint8_t> rs;
     rs.alloc(E + 1, st);
