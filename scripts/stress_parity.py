@@ -20,7 +20,8 @@ t_end = time.time() + secs
 n_checks = n_graphs = 0
 bad = []
 while time.time() < t_end:
-    nu, nv = int(rng.integers(1, 320)), int(rng.integers(1, 320))
+    hi = int(os.environ.get("STRESS_MAXN", "320"))
+    nu, nv = int(rng.integers(1, hi)), int(rng.integers(1, hi))
     t_graph = time.time()
     g = synth.random_bipartite(nu, nv, float(rng.uniform(0.003, 0.35)), int(rng.integers(1 << 30)))
     if rng.random() < 0.4 and nu > 8 and nv > 8:  # plant a dense block
