@@ -397,7 +397,7 @@ def main():
             "vs_baseline": None, "dtype": "u32-bitset/u128-count", "data": "synthetic",
             "config": {"workload": work, "config": args.config, "p": p, "q": q,
                        "anchor": "UV"[instr.anchor], "tasks": instr.tasks_emitted,
-                       "parallelism": f"task-shard{world}",
+                       "parallelism": f"root-shard{world}" + ("+2hop-shard" if world > 1 else ""),
                        "l2": "flushed between timed steps (256 MiB device write)"},
             "phases_ms": {"prep": 1e3 * statistics.mean(prep_s),
                           "level1": 1e3 * statistics.mean(level1_s),
