@@ -35,8 +35,10 @@ extern "C" {
 #define BC_ENCCL (-3)
 #define BC_EOOM (-4)
 #define BC_EOVERFLOW (-5)
+#define BC_EASSERT (-6)     /* BC_FLAG_CHECK_NESTING found a violation (the reference's
+                               AssertionError, engine.py:365-366) */
 
-#define BC_ABI_VERSION 2
+#define BC_ABI_VERSION 3
 
 /* EngineConfig (engine.py:43-61) plus the device-side knobs. */
 typedef struct bc_config {
@@ -61,6 +63,11 @@ typedef struct bc_config {
                              task, tasks in reference emission order (engine.py:160-172);
                              capacity in tasks given by task_counts_cap */
   int64_t task_counts_cap;
+  uint32_t *task_claims;  /* BC_FLAG_TRACK_TASKS: [tasks_emitted] how many times each task
+                             (reference emission order) was claimed by a warp; every entry
+                             of this shard's tasks must read 1 (EngineConfig.track_tasks,
+                             engine.py:446,462,473,498-499: task_tally is built from it) */
+  int64_t task_claims_cap;
 } bc_config;
 
 #define BC_FLAG_TASK_COUNTS 1   /* fill cfg->task_counts */
@@ -74,6 +81,12 @@ typedef struct bc_config {
 #define BC_FLAG_ROWR_PROBE 64   /* candidate rows by per-candidate intersections */
 #define BC_FLAG_TASK_SHARD 128  /* multi-GPU: tasks interleaved (t % shard_count) instead of
                                    whole roots dealt degree-balanced (the default) */
+#define BC_FLAG_TRACK_TASKS 256 /* fill cfg->task_claims (EngineConfig.track_tasks) */
+#define BC_FLAG_CHECK_NESTING 512 /* EngineConfig.check_nesting (engine.py:296-297,365-366):
+                                   for every task that descends, recompute every child
+                                   C_L = C_L1 & dir2(u) from the HTB arenas and check each id
+                                   against the root's directed 2-hop list; BC_EASSERT on a
+                                   violation */
 
 /* CountReport (engine.py:64-79) plus device measurements. */
 typedef struct bc_report {
@@ -82,7 +95,7 @@ typedef struct bc_report {
   int32_t anchor;                /* 0 = 'U', 1 = 'V' */
   int32_t p_eff, q_eff;
   int64_t tasks_emitted;         /* whole job, as engine.py:147-173 */
-  int64_t tasks_consumed;        /* tasks this shard ran */
+  int64_t tasks_consumed;        /* tasks this shard claimed (device counter) */
   int64_t tasks_stolen;          /* dynamic-queue claims beyond each warp's first */
   int64_t roots_filtered;
   int64_t batches_executed;      /* reference hybrid/dfs batch accounting */
@@ -98,6 +111,7 @@ typedef struct bc_report {
   double time_enum;              /* s: enumeration (time_2hop analogue) */
   double time_total;             /* s: whole call */
   int64_t level1_operand_words;  /* BC_FLAG_INSTRUMENT: the level-1 share of operand_words */
+  int64_t nesting_checked;       /* BC_FLAG_CHECK_NESTING: child C_L ids checked */
 } bc_report;
 
 /* Export ids for bc_export (device structures, for parity tests). */

@@ -13,10 +13,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # BC_LIB selects a development build (e.g. the phase-profiling one); default in-tree .so
 LIB_PATH = os.environ.get("BC_LIB") or os.path.join(HERE, "libbicount_b200.so")
 
-BC_OK, BC_EINVAL, BC_ECUDA, BC_ENCCL, BC_EOOM, BC_EOVERFLOW = 0, -1, -2, -3, -4, -5
+BC_OK, BC_EINVAL, BC_ECUDA, BC_ENCCL, BC_EOOM, BC_EOVERFLOW, BC_EASSERT = 0, -1, -2, -3, -4, -5, -6
+ABI_VERSION = 3
 BC_FLAG_TASK_COUNTS, BC_FLAG_INSTRUMENT, BC_FLAG_NO_SPLIT = 1, 2, 4
 BC_FLAG_L1_SCATTER, BC_FLAG_L1_PROBE, BC_FLAG_ROWR_SCATTER, BC_FLAG_ROWR_PROBE = 8, 16, 32, 64
-BC_FLAG_TASK_SHARD = 128
+BC_FLAG_TASK_SHARD, BC_FLAG_TRACK_TASKS, BC_FLAG_CHECK_NESTING = 128, 256, 512
 
 (BC_X_UND_SIZE, BC_X_RANK, BC_X_ORDER, BC_X_DIR_OFF, BC_X_DIR_IDX, BC_X_HADJ_OFF,
  BC_X_HADJ_IDX, BC_X_HADJ_VAL, BC_X_HDIR_OFF, BC_X_HDIR_IDX, BC_X_HDIR_VAL, BC_X_TASKS,
@@ -36,7 +37,8 @@ class BcConfig(C.Structure):
                 ("shard_count", C.c_int32), ("flags", C.c_int32),
                 ("rank_override", C.c_void_p), ("n_rank", C.c_int64),
                 ("roots", C.c_void_p), ("n_roots", C.c_int64),
-                ("task_counts", C.c_void_p), ("task_counts_cap", C.c_int64)]
+                ("task_counts", C.c_void_p), ("task_counts_cap", C.c_int64),
+                ("task_claims", C.c_void_p), ("task_claims_cap", C.c_int64)]
 
 
 class BcReport(C.Structure):
@@ -53,7 +55,7 @@ class BcReport(C.Structure):
                 ("d2h_bytes", C.c_int64), ("time_h2d", C.c_double),
                 ("time_prep", C.c_double), ("time_level1", C.c_double),
                 ("time_enum", C.c_double), ("time_total", C.c_double),
-                ("level1_operand_words", C.c_int64)]
+                ("level1_operand_words", C.c_int64), ("nesting_checked", C.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -134,7 +136,7 @@ def load():
     global _lib
     if _lib is None:
         L = open_library()
-        if L.bc_abi_version() != 2:
+        if L.bc_abi_version() != ABI_VERSION:
             raise RuntimeError("libbicount_b200.so ABI version mismatch")
         if L.bc_device_count() < 1:
             raise RuntimeError("no CUDA device visible: the B200 path has no CPU fallback")
@@ -148,4 +150,6 @@ def check(rc: int) -> None:
     msg = (_lib or open_library()).bc_last_error().decode(errors="replace")
     if rc == BC_EINVAL:
         raise ValueError(msg)
+    if rc == BC_EASSERT:  # check_nesting (the reference's assert, engine.py:365-366)
+        raise AssertionError(msg)
     raise RuntimeError(f"bicount_b200 error {rc}: {msg}")

@@ -47,13 +47,23 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// 128-bit accumulator as two u64 limbs (lo, hi) with explicit carry.
+// 128-bit accumulator as two u64 limbs (lo, hi) with explicit carry.  A carry out
+// of hi (a partial sum of terms that each fit 128 bits passing 2^128) latches `ovf`,
+// which atomic_add128 turns into the BC_EOVERFLOW flag: never a wrapped count.
 struct Acc128 {
   unsigned long long lo, hi;
+  unsigned ovf;
   __device__ __forceinline__ void add(unsigned long long xlo, unsigned long long xhi) {
-    unsigned long long n = lo + xlo;
-    hi += xhi + (n < lo ? 1ull : 0ull);
+    const unsigned long long n = lo + xlo;
+    const unsigned long long h1 = hi + xhi;
+    const unsigned long long h2 = h1 + (n < lo ? 1ull : 0ull);
+    ovf |= (h1 < hi) | (h2 < h1);
+    hi = h2;
     lo = n;
+  }
+  __device__ __forceinline__ void add(const Acc128 &o) {
+    add(o.lo, o.hi);
+    ovf |= o.ovf;
   }
 };
 
@@ -64,20 +74,33 @@ __device__ __forceinline__ Acc128 warp_sum128(Acc128 a) {
     unsigned long long h = __shfl_xor_sync(FULL, a.hi, o);
     a.add(l, h);
   }
+  a.ovf = __any_sync(FULL, a.ovf != 0) ? 1u : 0u;
   return a;
 }
 
 // Global 128-bit accumulation with carry; sets *overflow if the sum passes 2^128.
 __device__ __forceinline__ void atomic_add128(unsigned long long *lo_hi, int *overflow,
                                               unsigned long long lo, unsigned long long hi) {
+  unsigned long long carry = 0;
   if (lo) {
-    unsigned long long old = atomicAdd(lo_hi, lo);
-    if (old + lo < old) hi += 1;  // hi+1 cannot wrap unless hi == ~0: caught below
+    const unsigned long long old = atomicAdd(lo_hi, lo);
+    carry = old + lo < old ? 1ull : 0ull;
   }
-  if (hi) {
-    unsigned long long old = atomicAdd(lo_hi + 1, hi);
-    if (old + hi < old) atomicExch(overflow, 1);
+  if (hi | carry) {
+    const unsigned long long h = hi + carry;
+    if (h < hi) {  // hi == ~0 and a carry in: the sum is >= 2^128
+      atomicExch(overflow, 1);
+      return;
+    }
+    const unsigned long long old = atomicAdd(lo_hi + 1, h);
+    if (old + h < old) atomicExch(overflow, 1);
   }
+}
+
+__device__ __forceinline__ void atomic_add128(unsigned long long *lo_hi, int *overflow,
+                                              const Acc128 &a) {
+  if (a.ovf) atomicExch(overflow, 1);
+  atomic_add128(lo_hi, overflow, a.lo, a.hi);
 }
 
 // lower_bound over a sorted u32 array in [lo, hi).

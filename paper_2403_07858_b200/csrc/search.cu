@@ -68,22 +68,29 @@ using namespace sk;
 // ---------------------------------------------------------------------------
 __global__ void p1_kernel(Params P, const int64_t *__restrict__ deg_off) {
   Acc128 a{0, 0};
+  unsigned long long mine = 0;
   const int64_t nloc = P.n_local;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nloc;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int r = P.tasks[t].x;
     const int d = (int)(deg_off[r + 1] - deg_off[r]);
+    mine++;
+    if (P.claims) atomicAdd(P.claims + t, 1u);
     Acc128 one{0, 0};
     if (d >= P.q_eff) add_comb(P, one, d);
     if (P.task_counts) {
       P.task_counts[2 * t] = one.lo;
       P.task_counts[2 * t + 1] = one.hi;
     }
-    a.add(one.lo, one.hi);
+    a.add(one);
   }
   a = warp_sum128(a);
-  if (lane_id() == 0) atomic_add128(P.acc, P.overflow, a.lo, a.hi);
+  const unsigned long long consumed = warp_sum(mine);
+  if (lane_id() == 0) {
+    atomic_add128(P.acc, P.overflow, a);
+    if (consumed) atomicAdd(P.ctr + CTR_CONSUMED, consumed);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -97,10 +104,12 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nloc = P.n_local;
   Acc128 a{0, 0};
-  unsigned long long alive = 0, inter = 0, opw = 0, minw = 0, maxro = 0, maxscr = 0;
+  unsigned long long alive = 0, inter = 0, opw = 0, minw = 0, maxro = 0, maxscr = 0, claimed = 0;
   for (int64_t j = gw; j < nloc; j += nw) {
     const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
     const int2 tk = P.tasks[t];
+    claimed++;
+    if (P.claims && lane == 0) atomicAdd(P.claims + t, 1u);
     int cr, wr;
     if (P.lists) {  // C_R1 from the wedge-scatter pass: |C_R1| and its HTB word count
       const int64_t l0 = P.roff[j];
@@ -161,11 +170,12 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
         P.task_counts[2 * t + 1] = one.hi;
       }
     }
-    a.add(one.lo, one.hi);  // lane-uniform: only lane 0 contributes below
+    a.add(one);  // lane-uniform: only lane 0 contributes below
   }
   if (lane == 0) {
-    atomic_add128(P.acc, P.overflow, a.lo, a.hi);
+    atomic_add128(P.acc, P.overflow, a);
     if (alive) atomicAdd(P.ctr + CTR_ALIVE, alive);
+    if (claimed) atomicAdd(P.ctr + CTR_CONSUMED, claimed);
     if (INSTR) {
       atomicAdd(P.ctr + CTR_INTER, inter);
       atomicAdd(P.ctr + CTR_OPW, opw);
@@ -174,6 +184,70 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
     }
     if (maxro) atomicMax(P.ctr + CTR_MAXRO, maxro);
     if (maxscr) atomicMax(P.ctr + CTR_MAXSCR, maxscr);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// check_nesting (engine.py:296-297, 365-366): the reference asserts, for every
+// child it expands below level 1, that C_L' = C_L & dir2(u) is a subset of
+// dir2(root).  Every deeper C_L is an AND-subset of a level-2 set, so this
+// kernel recomputes every level-2 set of every task that descends -- C_L1 =
+// dir2(r) & dir2(s) and C_L1 & dir2(x) for each x in C_L1, from the HTB arenas
+// with the same warp intersection the search uses -- and checks each id against
+// the root's directed 2-hop list by binary search in the CSR (an independent
+// path).  Violations and checked ids are tallied; the host raises BC_EASSERT.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) nesting_check(Params P, const Info *__restrict__ info,
+                                                     const int64_t *__restrict__ dir_off,
+                                                     const int32_t *__restrict__ dir_idx,
+                                                     uint32_t *__restrict__ scratch, int64_t maxw) {
+  const int lane = lane_id();
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t *c_idx = scratch + gw * 3 * (maxw + 1);
+  uint32_t *c_val = c_idx + maxw + 1;
+  int *c_pre = (int *)(c_val + maxw + 1);
+  unsigned long long bad = 0, checked = 0;
+  for (int64_t j = gw; j < P.n_local; j += nw) {
+    const Info in = info[j];
+    if (in.cr < P.q_eff || in.cl < P.p_eff - 2) continue;  // no descent (prune_keep)
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
+    const int2 tk = P.tasks[t];
+    int cl = 0;
+    const int wl = isect_dir<true>(P.g, tk.x, tk.y, cl, c_idx, c_val, c_pre);
+    const int64_t r0 = dir_off[tk.x], r1 = dir_off[tk.x + 1];
+    for (int k = 0; k < wl; k++) {
+      uint32_t v = c_val[k];
+      while (v) {
+        const int x = (int)(c_idx[k] * 32u) + __ffs(v) - 1;
+        v &= v - 1;
+        const int64_t x0 = P.g.doff[x], x1 = P.g.doff[x + 1];
+        for (int b = lane; b < wl; b += 32) {
+          const uint32_t key = c_idx[b];
+          const int64_t i = lower_bound_u32(P.g.didx, x0, x1, key);
+          uint32_t w = i < x1 && __ldg(P.g.didx + i) == key ? c_val[b] & __ldg(P.g.dval + i) : 0u;
+          while (w) {
+            const int id = (int)(key * 32u) + __ffs(w) - 1;
+            w &= w - 1;
+            int64_t lo = r0, hi = r1;
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              if (__ldg(dir_idx + mid) < id) lo = mid + 1;
+              else hi = mid;
+            }
+            checked++;
+            if (!(lo < r1 && __ldg(dir_idx + lo) == id)) bad++;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  bad = warp_sum(bad);
+  checked = warp_sum(checked);
+  if (lane == 0) {
+    if (bad) atomicAdd(P.ctr + CTR_NEST_BAD, bad);
+    if (checked) atomicAdd(P.ctr + CTR_NEST_CHECKED, checked);
   }
 }
 
@@ -746,6 +820,13 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     tcounts.alloc(2 * (size_t)(n_tasks ? n_tasks : 1), st);
     tcounts.zero();
   }
+  DBuf<uint32_t> claims;
+  const bool want_claims = (cfg.flags & BC_FLAG_TRACK_TASKS) && cfg.task_claims;
+  if (want_claims) {
+    if (cfg.task_claims_cap < n_tasks) throw Error(BC_EINVAL, "task_claims buffer too small");
+    claims.alloc((size_t)(n_tasks ? n_tasks : 1), st);
+    claims.zero();
+  }
   Params P;
   P.g = Graph2{s.hadj_off.p, s.hadj_idx.p, s.hadj_val.p, s.hdir_off.p, s.hdir_idx.p, s.hdir_val.p,
                s.dense_id.p, s.dense.p, s.dense_mw, s.boff, s.bidx};
@@ -765,6 +846,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.overflow = ovf.p;
   P.ctr = ctr.p;
   P.task_counts = want_tc ? tcounts.p : nullptr;
+  P.claims = want_claims ? claims.p : nullptr;
   P.roff = nullptr;
   P.lists = nullptr;
   P.rowR_mode = (cfg.flags & BC_FLAG_ROWR_SCATTER) ? 1 : (cfg.flags & BC_FLAG_ROWR_PROBE) ? 2 : 0;
@@ -934,6 +1016,15 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       launches++;
     }
     BC_CUDA(cudaEventRecord(e1, st));
+    if ((cfg.flags & BC_FLAG_CHECK_NESTING) && s.p_eff >= 4) {
+      const int64_t maxw = std::max<int64_t>(s.max_dir_slice, 1);
+      const int nb = sms * 2;
+      DBuf<uint32_t> scr;
+      scr.alloc((size_t)nb * 8 * 3 * (maxw + 1), st);
+      nesting_check<<<nb, 256, 0, st>>>(P, info.p, s.dir_off.p, s.dir_idx.p, scr.p, maxw);
+      BC_CHECK_LAUNCH();
+      launches++;
+    }
     if (s.p_eff >= 3) {
       unsigned long long h[CTR_COUNT];
       copy_d2h(h, ctr.p, sizeof h, st);
@@ -1348,6 +1439,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   copy_d2h(h_ctr, ctr.p, sizeof h_ctr, st);
   copy_d2h(&h_ovf, ovf.p, sizeof h_ovf, st);
   if (want_tc) copy_d2h(cfg.task_counts, tcounts.p, 2 * n_tasks * sizeof(uint64_t), st);
+  if (want_claims) copy_d2h(cfg.task_claims, claims.p, n_tasks * sizeof(uint32_t), st);
   BC_CUDA(cudaStreamSynchronize(st));
   float t1 = 0, t2 = 0;
   BC_CUDA(cudaEventElapsedTime(&t1, e0, e1));
@@ -1356,10 +1448,15 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
   if (h_ovf == 2) throw Error(BC_ECUDA, "enumeration frame exceeded its scratch sizing");
+  if (h_ctr[CTR_NEST_BAD])
+    throw Error(BC_EASSERT, "check_nesting: " + std::to_string(h_ctr[CTR_NEST_BAD]) + " of " +
+                                std::to_string(h_ctr[CTR_NEST_CHECKED]) +
+                                " child C_L ids are outside dir2(root)");
   out.count_lo = h_acc[0];
   out.count_hi = h_acc[1];
   out.overflow = h_ovf ? 1 : 0;
-  out.tasks_consumed = nloc;
+  out.tasks_consumed = (int64_t)h_ctr[CTR_CONSUMED];
+  out.nesting_checked = (int64_t)h_ctr[CTR_NEST_CHECKED];
   out.tasks_alive = n_alive;
   out.tasks_split = n_split;
   out.tasks_stolen = (int64_t)h_ctr[CTR_STOLEN];

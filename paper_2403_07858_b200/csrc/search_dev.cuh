@@ -85,7 +85,9 @@ struct Params {
   const int32_t *__restrict__ lists;    //   lists[roff[j], roff[j+1]) (ascending ids), or null
   int rowR_mode;                        // 0 = per-task choice, 1 = scatter, 2 = probe
   const int64_t *__restrict__ ltask;    // root sharding: global id of local task j (or null:
-};                                      //   task interleave t = shard + j * nshards)
+                                        //   task interleave t = shard + j * nshards)
+  unsigned *claims;                     // optional [n_tasks]: claims per task (track_tasks)
+};
 
 // global task id of this shard's local task j
 __host__ __device__ __forceinline__ int64_t task_id(const int64_t *ltask, int shard, int nshards,
@@ -95,7 +97,7 @@ __host__ __device__ __forceinline__ int64_t task_id(const int64_t *ltask, int sh
 
 enum { CTR_ALIVE = 0, CTR_BATCHES, CTR_STOLEN, CTR_INTER, CTR_OPW, CTR_MINW, CTR_MAXRO,
        CTR_MAXSCR, CTR_SPILL, CTR_NEXT, CTR_SUB_USED, CTR_SUB_N, CTR_SUB_NEXT, CTR_SPLIT,
-       CTR_HEAVY, CTR_OPW_L1, CTR_COUNT };
+       CTR_HEAVY, CTR_OPW_L1, CTR_CONSUMED, CTR_NEST_BAD, CTR_NEST_CHECKED, CTR_COUNT };
 
 struct Info {  // level-1 facts of one task
   int32_t cr, wr, cl, wl;
@@ -1390,9 +1392,9 @@ __device__ __forceinline__ void finish_task(const Params &P, Acc128 acc, int64_t
                                             Acc128 &total) {
   acc = warp_sum128(acc);
   if (lane_id() == 0) {
-    total.add(acc.lo, acc.hi);
+    total.add(acc);
     if (P.task_counts) {
-      if (atomic) atomic_add128(P.task_counts + 2 * t, P.overflow, acc.lo, acc.hi);
+      if (atomic) atomic_add128(P.task_counts + 2 * t, P.overflow, acc);
       else {
         P.task_counts[2 * t] = acc.lo;
         P.task_counts[2 * t + 1] = acc.hi;
@@ -1408,7 +1410,7 @@ __device__ __forceinline__ void flush_tallies(const Params &P, const Acc128 &tot
   const int lane = lane_id();
   const unsigned long long batches = warp_sum(tl.batches);  // leaf_parents tally per lane
   if (lane == 0) {
-    atomic_add128(P.acc, P.overflow, total.lo, total.hi);
+    atomic_add128(P.acc, P.overflow, total);
     atomicAdd(P.ctr + CTR_BATCHES, batches);
     if (claims > 1) atomicAdd(P.ctr + CTR_STOLEN, claims - 1);
     if (spills) atomicAdd(P.ctr + CTR_SPILL, spills);

@@ -369,6 +369,38 @@ def _report(rep: _abi.BcReport, cfg: EngineConfig, wall: float, anchor_layer: st
         task_counts=per_task, device=d)
 
 
+def task_bound(u_off, u_idx, v_off, v_idx, p: int) -> int:
+    """Upper bound on tasks_emitted for either anchor layer, from host CSR: one task per
+    anchor when p_eff = 1, else one per directed 2-hop pair, and an anchor's undirected
+    2-hop list holds at most min(n - 1, sum over its neighbours v of deg(v) - 1) ids
+    (graph.py:192-224), each pair counted from both ends."""
+    best = 0
+    for aoff, aidx, boff in ((u_off, u_idx, v_off), (v_off, v_idx, u_off)):
+        n = len(aoff) - 1
+        if p <= 1 or n == 0:
+            best = max(best, n)
+            continue
+        dm1 = np.diff(boff) - 1
+        per = np.zeros(n, dtype=np.int64)
+        if len(aidx):
+            w = np.concatenate([[0], np.cumsum(dm1[aidx], dtype=np.int64)])
+            per = w[aoff[1:]] - w[aoff[:-1]]
+        best = max(best, int((np.minimum(per, n - 1).sum() + 1) // 2), n)
+    return best
+
+
+def task_tally(claims: np.ndarray, emitted: int, workers: int):
+    """(task_tally, task_counts) in the reference's terms (engine.py:446,462,473,498-499):
+    task t of the round-robin emission is entry (t % workers, t // workers); the device
+    logs how many times each task was claimed, so a task run twice appears twice and a
+    task never run does not appear."""
+    c = claims[:emitted].astype(np.int64)
+    t = np.repeat(np.arange(emitted, dtype=np.int64), c)
+    tally = list(zip((t % workers).tolist(), (t // workers).tolist()))
+    counts = [(emitted - w + workers - 1) // workers for w in range(workers)]
+    return tally, counts
+
+
 def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
                     structures=None, roots=None) -> CountReport:
     """Exact (p,q)-biclique count on the GPU (engine.py:419-500).
@@ -377,7 +409,12 @@ def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
     anchor layer and the priority rank, as in the reference's partitioned
     counting (partition.py:246-249); the device rebuilds the rest itself.
     ``roots`` restricts which anchor vertices root tasks (engine.py:155-162).
-    ``wall_time`` covers the device call (preprocessing + counting).
+    ``wall_time`` covers the counting phase (level 1 + enumeration, device
+    events), not structure preparation, as in the reference (engine.py:432,492);
+    ``device["time_total"]`` is the whole call.  ``track_tasks`` fills
+    ``task_tally`` / ``task_counts`` from the device's per-task claim log;
+    ``check_nesting`` runs the device nesting check (AssertionError on a
+    violation, as the reference's assert, engine.py:365-366).
     """
     cfg = cfg if cfg is not None else EngineConfig()
     cfg.validate()
@@ -392,31 +429,40 @@ def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
         rank = np.asarray(structures.order.rank, dtype=np.int64)
     L = _abi.load()
     (uo, ui, vo, vi), nu, nv = _csr_arrays(graph)
-    c, keep = _make_config(cfg, anchor, rank, roots)
+    flags = (_abi.BC_FLAG_TRACK_TASKS if cfg.track_tasks else 0) | (
+        _abi.BC_FLAG_CHECK_NESTING if cfg.check_nesting else 0)
+    c, keep = _make_config(cfg, anchor, rank, roots, flags=flags)
+    claims = None
+    if cfg.track_tasks:
+        cap = max(1, task_bound(uo, ui, vo, vi, int(pp)))
+        claims = np.zeros(cap, dtype=np.uint32)
+        c.task_claims = claims.ctypes.data
+        c.task_claims_cap = cap
     rep = _abi.BcReport()
-    t0 = perf_counter()
     _abi.check(L.bc_count(uo.ctypes.data, ui.ctypes.data, nu, vo.ctypes.data, vi.ctypes.data, nv,
                           int(pp), int(qq), C.byref(c), C.byref(rep)))
-    wall = perf_counter() - t0
     del keep
     layer = structures.choice.layer if structures is not None else "UV"[rep.anchor]
-    out = _report(rep, cfg, wall, layer)
+    out = _report(rep, cfg, rep.time_level1 + rep.time_enum, layer)
+    if claims is not None:
+        out.task_tally, out.task_counts = task_tally(claims, rep.tasks_emitted, cfg.worker_count)
     if cfg.enumerate_results:
-        if roots is not None or structures is not None:
-            raise ValueError("enumerate_results does not combine with roots= / structures=")
-        out.bicliques = enumerate_bicliques(graph, pp, qq, cfg, out.count, layer)
+        out.bicliques = enumerate_bicliques(graph, pp, qq, cfg, out.count, layer, anchor=anchor,
+                                            rank=rank, roots=roots)
     return out
 
 
 ENUM_GUARD = 10**7
 
 
-def enumerate_bicliques(g, p: int, q: int, cfg: EngineConfig, count: int, layer: str):
+def enumerate_bicliques(g, p: int, q: int, cfg: EngineConfig, count: int, layer: str, *,
+                        anchor=None, rank=None, roots=None):
     """Every (p,q)-biclique as (L, R) tuples, sorted (engine.py:301-304, 480-483).
 
     The search runs on the GPU (``bc_graph_enumerate``: one record per leaf, [L, |C_R|,
     C_R]); the host only expands each record into combinations(C_R, q_eff), swaps the
-    pair for a V anchor and sorts."""
+    pair for a V anchor and sorts.  ``anchor`` / ``rank`` / ``roots`` as in
+    ``count_bicliques`` (a caller's ``structures`` fixes the first two)."""
     from itertools import combinations
 
     if count > ENUM_GUARD:
@@ -424,7 +470,7 @@ def enumerate_bicliques(g, p: int, q: int, cfg: EngineConfig, count: int, layer:
     L = _abi.load()
     dg = DeviceGraph(g, cfg.device)
     try:
-        c, keep = _make_config(cfg, cfg.anchor, None, None)
+        c, keep = _make_config(cfg, anchor or cfg.anchor, rank, roots)
         need = C.c_int64(0)
         cap = 1 << 16
         while True:
@@ -506,13 +552,16 @@ def assemble_upper(slices):
     return off, ids
 
 
-def assemble_upper_device(lens_all, ids_all, stride: int, n_pairs: int, device: int = 0):
+def assemble_upper_device(lens_all, ids_all, stride: int, n_pairs: int, device: int = 0, *,
+                          world: int):
     """``assemble_upper`` on the device (bc_assemble_upper): lens_all int32[world * n],
     ids_all int32[world * stride] (rank r's slice ids at r * stride)."""
     import torch
 
     L = _abi.load()
-    world = ids_all.numel() // max(stride, 1) if stride else lens_all.numel()
+    if world < 1 or stride < 1 or lens_all.numel() % world or ids_all.numel() < world * stride:
+        raise ValueError("assemble_upper_device: need world >= 1, stride >= 1, "
+                         "lens_all of world * n entries and ids_all of world * stride")
     n = lens_all.numel() // world
     off = torch.empty(n + 1, dtype=torch.int64, device=lens_all.device)
     ids = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=lens_all.device)
@@ -545,7 +594,7 @@ def gather_upper(dg: DeviceGraph, p: int, q: int, cfg: EngineConfig, rank: int, 
     dist.all_gather(all_lens, lens.to(cdev), group=group)
     total = sum(int(x.item()) for x in sizes)
     return assemble_upper_device(torch.cat(all_lens).to(dev), torch.cat(all_ids).to(dev),
-                                 pad.numel(), total, dev.index or 0)
+                                 pad.numel(), total, dev.index or 0, world=world)
 
 
 def count_bicliques_distributed(g, p: int, q: int, cfg: EngineConfig | None = None, *,

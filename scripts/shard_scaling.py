@@ -58,7 +58,7 @@ for n in (1, 2, 4, 8):
         for _ in range(2):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            upper = assemble_upper_device(lens_all, ids_all, stride, total_pairs)
+            upper = assemble_upper_device(lens_all, ids_all, stride, total_pairs, world=n)
             torch.cuda.synchronize()
             asm_ms = 1e3 * (time.perf_counter() - t0)
     for k in range(n):

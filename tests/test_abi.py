@@ -35,15 +35,35 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_device_probe(lib):
-    assert lib.bc_abi_version() == 2
+    assert lib.bc_abi_version() == _abi.ABI_VERSION == 3
     assert lib.bc_device_count() >= 0
 
 
 def test_struct_layout_matches_header():
-    # bc_config: 8 x int32, then ptr/int64 pairs x 3 -> 32 + 48 = 80 bytes
-    assert C.sizeof(_abi.BcConfig) == 80
-    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 + 1 i64 = 16 + 16 + 144 + 40 + 8
-    assert C.sizeof(_abi.BcReport) == 224
+    # bc_config: 8 x int32, then ptr/int64 pairs x 4 -> 32 + 64 = 96 bytes
+    assert C.sizeof(_abi.BcConfig) == 96
+    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 + 2 i64 = 16 + 16 + 144 + 40 + 16
+    assert C.sizeof(_abi.BcReport) == 232
+    # and the C compiler agrees with ctypes on every field offset
+    import subprocess
+    import tempfile
+
+    fields = [("bc_config", f) for f, _ in _abi.BcConfig._fields_] + [
+        ("bc_report", f) for f, _ in _abi.BcReport._fields_]
+    src = "#include <stdio.h>\n#include <stddef.h>\n#include \"bicount_b200.h\"\nint main(void){\n"
+    src += 'printf("%zu %zu\\n", sizeof(bc_config), sizeof(bc_report));\n'
+    for st, f in fields:
+        src += f'printf("%zu\\n", offsetof({st}, {f}));\n'
+    src += "return 0;}\n"
+    with tempfile.TemporaryDirectory() as d:
+        c_file, exe = os.path.join(d, "t.c"), os.path.join(d, "t")
+        open(c_file, "w").write(src)
+        subprocess.run(["gcc", "-I", os.path.dirname(HEADER), "-o", exe, c_file], check=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()
+    assert [int(x) for x in out[:2]] == [C.sizeof(_abi.BcConfig), C.sizeof(_abi.BcReport)]
+    want = [getattr(_abi.BcConfig, f).offset for _, f in fields[:len(_abi.BcConfig._fields_)]]
+    want += [getattr(_abi.BcReport, f).offset for _, f in fields[len(_abi.BcConfig._fields_):]]
+    assert [int(x) for x in out[2:]] == want
     text = open(HEADER).read()
     cfg_body = re.search(r"typedef struct bc_config \{(.*?)\} bc_config;", text, re.S).group(1)
     names = re.findall(r"\*?(\w+)\s*(?:,|;)", re.sub(r"/\*.*?\*/", "", cfg_body, flags=re.S))

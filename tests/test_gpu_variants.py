@@ -146,6 +146,22 @@ def test_u128_counts_and_overflow():
         count_bicliques(g, 2, 40)  # C(200,2) * C(200,40) > 2^128
 
 
+@pytest.mark.parametrize("p", [1, 2])
+def test_u128_sum_overflow_of_small_terms(p):
+    """Every term C(131, 65) < 2^128, but three of them pass 2^128: the per-warp and
+    global 128-bit sums must report the overflow, not wrap (K_{3,131})."""
+    from math import comb
+
+    nu, nv = 3, 131
+    k = np.arange(nu * nv)
+    g = synth.from_edges(nu, nv, k // nv, k % nv)
+    assert comb(131, 65) < 2**128 <= 3 * comb(131, 65)
+    with pytest.raises(RuntimeError, match="128 bits"):
+        count_bicliques(g, p, 65, EngineConfig(anchor="U"))
+    g1 = synth.from_edges(1, nv, np.zeros(nv, np.int64), np.arange(nv))
+    assert count_bicliques(g1, 1, 65, EngineConfig(anchor="U")).count == comb(131, 65)
+
+
 def test_enumeration_matches_brute_force():
     """enumerate_results (reference engine.py:301-304, 480-483): the device search emits
     every biclique; sorted (L, R) pairs equal an independent brute-force enumeration,
@@ -261,7 +277,7 @@ def test_assemble_upper_device_matches_host():
         for k, x in enumerate(sl):
             ids_all[k * stride:k * stride + x[1].numel()] = x[1]
         off, ids = assemble_upper_device(torch.cat([x[0] for x in sl]), ids_all, stride,
-                                         sum(x[1].numel() for x in sl))
+                                         sum(x[1].numel() for x in sl), world=n)
         off2, ids2 = assemble_upper(sl)
         assert torch.equal(off, off2) and torch.equal(ids, ids2)
     dg.close()
