@@ -1,23 +1,28 @@
 """Benchmark: exact (p,q)-biclique counting on B200 (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
 
-A step is one full counting pass of the hot path (device preprocessing:
-anchor choice, 2-hop index, priority, directed lists, HTB; then level-1 pass
-and hybrid DFS-BFS enumeration) over the named synthetic config.  Default
-workload: BASELINE configs[1] = C2, Chung-Lu 100K x 50K, 1M edges, (4,4).
+A step is one full counting pass of the hot path (device preprocessing: anchor choice,
+2-hop index, priority, directed lists, HTB; then the level-1 pass and the hybrid DFS-BFS
+enumeration) over the named synthetic config.  Default workload: C5, the FR-shaped
+(8,8) config (44K x 8.956M, 1e8 edges) -- the largest BASELINE config, and it fits one
+B200, so it is the N = 1 headline; C1-C4 are parity cases (``--config`` runs them too).
 
-* value  = bicliques/s of the whole job (all ranks), CSR already in HBM.
-* e2e    = same metric through the C-ABI bc_count from pinned HOST CSR
-           buffers (H2D + preprocessing + count + D2H inside the timing).
-* roofline = the search phase (level1_kernel + enum_kernel): B_enum
-           (8 B x sum(|a|+|b|) over the reference's HTB
-           intersections, tallied on device) / search time, vs measured HBM.
-* cpu_baseline = the CPU oracle port (oracle/, C + pthreads, all host cores).
+* value    = bicliques/s of the whole job (all ranks), CSR already in HBM, CUDA events.
+* e2e      = the same metric through the C-ABI ``bc_count`` from pinned HOST CSR buffers
+             (H2D + preprocessing + count + D2H inside the timing).
+* roofline = the enumeration kernels of one step (the dominant phase): their DRAM bytes
+             from an ncu capture of this exact build (profiles/r2/traffic.json, keyed by
+             the source hash) / their in-run CUDA-event time, vs the measured HBM peak;
+             beside it the compulsory bytes (each input they read, once) and the
+             reference's merge-equivalent operand bytes B_enum.
+* cpu_baseline = the CPU oracle port (oracle/, C + pthreads, every host core), on a
+             bounded sample when the full count is hours (C5), extrapolated by task share.
 
 Multi-GPU (torchrun): each rank builds the upper 2-hop lists of its share of the anchors,
-the slices are all-gathered over NCCL, and each rank counts its shard of the tasks (whole
-roots, degree-balanced); one NCCL all_reduce of four 32-bit limbs sums the exact partials.
+the slices are all-gathered (NCCL over NVLink), each rank counts its shard of the tasks
+(whole roots, degree-balanced), and one all_reduce of four 32-bit limbs sums the exact
+partials.  ``--dist-backend gloo`` runs the same ranks on one GPU (tests).
 """
 
 from __future__ import annotations
@@ -41,19 +46,33 @@ CONFIG_DESC = {
     "C3": "C3 GitHub-shaped Chung-Lu 56,519 x 120,867, 440,237 edges",
     "C4": "C4 S2-shaped synth 12,720 x 11,100 + 3 planted dense cores",
     "C5": "C5 FR-shaped capped Chung-Lu 44K x 8.956M, 1e8 edges + planted cores",
+    "C5H": "C5H FR-shaped capped Chung-Lu 44K x 8.956M, 1e8 edges + heavy planted cores",
 }
+DEVICE_GENERATED = ("C5", "C5H")  # built on the GPU by the integer counter-based recipe
 METRIC = "(p,q)-biclique count time (s) and bicliques/s at 1/2/4/8 B200 vs CPU ref"
 # batch_buffer_capacity per config: the reference rejects capacities below the largest
 # HTB slice (engine.py:387-391); C5's hub rows have 122,855 words (SURVEY 8(d) CPU timing
 # uses max(4096, max slice) the same way)
-CAPACITY = {"C5": 1 << 17}
-# CPU legs on C5 time the full CPU preprocessing plus the counting of a seeded sample of
-# roots, extrapolated by task share (a full CPU run is hours, SURVEY 7 hard part 6)
-SAMPLE_FRAC = {"C5": 0.005}
-# C5 (8,8) total, validated by the sampled-root parity test (tests/test_c5.py); used only
-# by the CPU-only reference arm, which cannot count C5 in full
-C5_COUNT = 9415393375594
+CAPACITY = {"C5": 1 << 17, "C5H": 1 << 17}
+# CPU legs on C5: the full CPU preprocessing plus the counting of a seeded sample of
+# roots, extrapolated by task share (a full CPU count is hours; tests/golden/c5_full.json
+# holds the one full offline run)
+SAMPLE_FRAC = {"C5": 0.002, "C5H": 0.002}
 FALLBACK_HBM = 6650.0
+ENUM_KERNELS = ("enum_kernel", "sub_kernel", "filter_kernel")
+
+
+def golden_count(config: str, p: int, q: int):
+    """The config's exact total as pinned by the reference (tests/golden/golden.json,
+    C1-C4) or by the full offline CPU oracle run (tests/golden/c5_full.json), else None."""
+    try:
+        if config in DEVICE_GENERATED:
+            d = json.load(open(os.path.join(ROOT, "tests", "golden", f"{config.lower()}_full.json")))
+            return int(d["count"]) if (d["p"], d["q"]) == (p, q) else None
+        d = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+        return int(d["configs"][config][f"({p},{q})"]["hybrid"]["count"])
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def env_int(k, d):
@@ -143,17 +162,39 @@ def measured_peak():
 
 def traffic_for(workload: str):
     """DRAM / L2 bytes of the enumeration kernels of one step, from the committed ncu
-    launch list of the same workload (profiles/traffic.json)."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+    launch list of this workload captured on THIS build (profiles/r2/traffic.json; the
+    entry is used only when its source hash equals the built sources')."""
+    from paper_2403_07858_b200 import build
+
+    p = os.path.join(ROOT, "profiles", "r2", "traffic.json")
     try:
         t = json.load(open(p)).get(workload)
     except (OSError, ValueError):
-        return None
-    return t if isinstance(t, dict) else None
+        return None, "no capture"
+    if not isinstance(t, dict):
+        return None, "no capture of this workload"
+    if t.get("src_sha") != build.source_hash():
+        return None, f"capture is of another build ({t.get('src_sha')})"
+    return t, t.get("source", "profiles/r2/traffic.json")
 
 
-def cpu_oracle_run(g, p, q, threads: int, config: str = ""):
-    """(count, seconds, sample description) of the CPU restatement on this host."""
+def sample_roots(prep, frac: float, seed: int):
+    """A seeded sample of anchor roots and its share of the emitted tasks."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    und = prep.export(O.X_UND_SIZE)
+    dsz = np.diff(prep.export(O.X_DIR_OFF))
+    ntask = np.where(und >= prep.p_eff - 1, dsz, 0)
+    roots = np.random.default_rng(seed).choice(prep.n, max(1, int(frac * prep.n)), replace=False)
+    return roots, float(ntask[roots].sum()) / float(max(1, ntask.sum()))
+
+
+def cpu_oracle_run(g, p, q, threads: int, config: str, seed: int = 1, prep_cache=None):
+    """(count or None, seconds, sample description) of the CPU restatement on this host.
+    Sampled configs: the preprocessing time (measured once, cached) plus the counting of a
+    seeded root sample extrapolated by its task share."""
     from oracle import oracle as O
 
     frac = SAMPLE_FRAC.get(config)
@@ -162,54 +203,93 @@ def cpu_oracle_run(g, p, q, threads: int, config: str = ""):
         t0 = time.perf_counter()
         r = O.count(g, p, q, workers=threads, threads=threads, capacity=cap)
         return r.count, time.perf_counter() - t0, "full count incl. preprocessing"
-    import numpy as np
-
-    t0 = time.perf_counter()
-    prep = O.Prepared(g, p, q, threads=threads)
-    t_prep = time.perf_counter() - t0
-    und = prep.export(O.X_UND_SIZE)
-    dsz = np.diff(prep.export(O.X_DIR_OFF))
-    ntask = np.where(und >= prep.p_eff - 1, dsz, 0)
-    roots = np.random.default_rng(1).choice(prep.n, max(1, int(frac * prep.n)), replace=False)
-    share = float(ntask[roots].sum()) / float(max(1, ntask.sum()))
+    cache = prep_cache if prep_cache is not None else {}
+    if "prep" not in cache:
+        t0 = time.perf_counter()
+        cache["prep"] = O.Prepared(g, p, q, threads=threads)
+        cache["t_prep"] = time.perf_counter() - t0
+    prep, t_prep = cache["prep"], cache["t_prep"]
+    roots, share = sample_roots(prep, frac, seed)
     t1 = time.perf_counter()
-    r = O.count(g, p, q, workers=threads, threads=threads, capacity=cap, roots=roots,
-                prepared=prep)
+    O.count(g, p, q, workers=threads, threads=threads, capacity=cap, roots=roots, prepared=prep)
     t_cnt = time.perf_counter() - t1
     est = t_prep + t_cnt / max(share, 1e-12)
     return None, est, (f"full CPU preprocessing ({t_prep:.1f} s) + counting {len(roots)} seeded "
-                       f"random roots ({100 * share:.2f}% of tasks, {t_cnt:.1f} s), "
+                       f"random roots ({100 * share:.3f}% of tasks, {t_cnt:.1f} s), "
                        f"extrapolated by task share")
 
 
-def run_reference(args, g, p, q, rank, world):
-    """--impl reference: the CPU restatement of the reference path (oracle/,
-    C + pthreads, every host core), rank 0 only."""
+def load_graph(config: str, device: int | None):
+    """(host BipartiteGraph, device CSR tensors or None)."""
+    from paper_2403_07858_b200 import synth
+
+    if config in DEVICE_GENERATED:
+        import torch
+
+        if device is None:
+            csr = synth.build_device_config(config, "cpu")
+            return synth.graph_from_torch_csr(*csr), None
+        csr = synth.build_device_config(config, f"cuda:{device}")
+        return synth.graph_from_torch_csr(*csr), csr
+    return synth.build_config(config), None
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU restatement of the reference path (oracle/, C + pthreads,
+    every host core), rank 0 only; each step is a bounded sample on sampled configs."""
     if rank != 0:
         return
+    from paper_2403_07858_b200 import synth
+
+    g, _ = load_graph(args.config, None)
+    p, q = pq_of(args)
     threads = host_cores()
-    for _ in range(args.warmup):
-        cpu_oracle_run(g, p, q, threads, args.config)
+    cache = {}
+    for i in range(args.warmup):
+        cpu_oracle_run(g, p, q, threads, args.config, seed=1000 + i, prep_cache=cache)
     times, count, what = [], None, ""
-    for _ in range(args.steps):
-        c, dt, what = cpu_oracle_run(g, p, q, threads, args.config)
+    for i in range(args.steps):
+        c, dt, what = cpu_oracle_run(g, p, q, threads, args.config, seed=1 + i, prep_cache=cache)
         times.append(dt)
-        count = c if c is not None else C5_COUNT
+        count = c if c is not None else golden_count(args.config, p, q)
     t = statistics.mean(times)
-    v = count / t
+    v = count / t if count else None
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "bicliques/s",
         "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
-        "time_s": t, "count": count, "higher_is_better": True, "scaling": "weak",
+        "time_s": t, "count": count, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"{CONFIG_DESC[args.config]} ({p},{q})", "config": args.config,
                    "p": p, "q": q},
         "cpu_baseline": {"value": v, "unit": "bicliques/s", "cores": threads, "kind": "port",
                          "sample": f"{args.config} ({p},{q}): {what} (oracle/bicount_oracle.c, "
-                                   f"{threads} pthreads, {cpu_model()})"},
+                                   f"{threads} pthreads, {cpu_model()}); count from "
+                                   + ("the run" if SAMPLE_FRAC.get(args.config) is None else
+                                      f"tests/golden/{args.config.lower()}_full.json")},
         "e2e": {"value": v, "unit": "bicliques/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    del synth
+
+
+def pq_of(args):
+    from paper_2403_07858_b200 import synth
+
+    pq = synth.CONFIGS[args.config][1][0]
+    return args.p or pq[0], args.q or pq[1]
+
+
+def compulsory_bytes(r, m: int, e: int) -> int:
+    """Bytes the enumeration kernels must read at least once (each input once, no
+    re-reads): the level-1 facts (16 B/task) and LPT queue (4 B/alive task), the C_R1
+    lists of the wedge-scatter level 1 (4 B/entry), the opposite-layer CSR the candidate
+    rows are built from (8 B/row offset + 4 B/id), the directed 2-hop HTB (8 B/word),
+    and the adjacency HTB (8 B/word) when level 1 probes instead of scattering."""
+    b = 16 * r.tasks_consumed + 4 * r.tasks_alive + 4 * r.level1_entries
+    b += 8 * (m + 1) + 4 * e + 8 * r.dir2_words
+    if r.level1_entries == 0:
+        b += 8 * r.adj_words
+    return int(b)
 
 
 def main():
@@ -217,10 +297,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -229,25 +310,8 @@ def main():
         args.warmup = 3
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    from paper_2403_07858_b200 import synth
-
-    dev_csr = None
-    if args.config == "C5" and args.impl == "ours":
-        import torch
-
-        # FR-shaped C5 is generated on the GPU (integer counter-based recipe, bit-identical
-        # on CPU); the host copy feeds the e2e leg and the CPU baseline
-        torch.cuda.set_device(env_int("LOCAL_RANK", 0))
-        dev_csr = synth.fr_shaped_csr(device="cuda")
-        g = synth.graph_from_torch_csr(*dev_csr)
-    else:
-        g = synth.build_config(args.config)
-    pq = synth.CONFIGS[args.config][1][0]
-    p = args.p or pq[0]
-    q = args.q or pq[1]
-
     if args.impl == "reference":
-        return run_reference(args, g, p, q, rank, world)
+        return run_reference(args, rank)
 
     import torch
     import torch.distributed as dist
@@ -256,10 +320,18 @@ def main():
     from paper_2403_07858_b200.engine import (DeviceGraph, EngineConfig, gather_upper, merge_limbs,
                                               split_limbs)
 
+    gloo = args.dist_backend == "gloo"
+    local = local % max(torch.cuda.device_count(), 1)  # gloo: several ranks may share a GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    cdev = torch.device("cpu") if gloo else dev
+    g, dev_csr = load_graph(args.config, local)
+    p, q = pq_of(args)
 
     def barrier():
         if world > 1:
@@ -268,14 +340,14 @@ def main():
     def allreduce_max(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def allreduce_count(c: int) -> int:
         if world == 1:
             return c
-        t = torch.tensor(split_limbs(c), dtype=torch.int64, device=dev)
+        t = torch.tensor(split_limbs(c), dtype=torch.int64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return merge_limbs(t.cpu().tolist())
 
@@ -283,6 +355,7 @@ def main():
     cfg = EngineConfig(device=local, batch_buffer_capacity=cap)
     dg = DeviceGraph.from_device_csr(*dev_csr, local) if dev_csr is not None else DeviceGraph(g, local)
     del dev_csr
+    torch.cuda.empty_cache()
     shard = (rank, world)
 
     def step():
@@ -302,7 +375,7 @@ def main():
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     step_ms, search_s, level1_s, enum_s, prep_s, launches = [], [], [], [], [], 0
-    count_local = None
+    count_local, last = None, None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -321,16 +394,23 @@ def main():
             prep_s.append(rep.time_prep)
             launches += rep.kernel_launches
             count_local = int(rep.count_lo) | (int(rep.count_hi) << 64)
+            last = rep
     clocks = clk.summary()
     barrier()
     ms_local = statistics.mean(step_ms)
     ms = allreduce_max(ms_local)
     total = allreduce_count(count_local)
-    t_search = allreduce_max(statistics.mean(search_s))
     t_enum = allreduce_max(statistics.mean(enum_s))
     b_enum = allreduce_count(b_enum_local)
     b_l1 = allreduce_count(b_l1_local)
     b_min = allreduce_count(b_min_local)
+    comp_local = compulsory_bytes(last, g.v_count if last.anchor == 0 else g.u_count,
+                                  g.edge_count)
+    comp = allreduce_count(comp_local) if world > 1 else comp_local
+    launches_all = allreduce_count(launches)
+    want = golden_count(args.config, p, q)
+    if want is not None and total != want:
+        raise SystemExit(f"count {total} differs from the pinned golden {want}")
 
     # e2e through the C-ABI from pinned host buffers
     e2e = None
@@ -342,10 +422,9 @@ def main():
         c.batch_words, c.mode, c.anchor, c.order_mode, c.device = cap, 1, -1, 0, local
         c.shard_index, c.shard_count, c.flags = rank, world, 0
         r = _abi.BcReport()
-        for _ in range(1):
-            _abi.check(L.bc_count(pinned[0].data_ptr(), pinned[1].data_ptr(), u.n,
-                                  pinned[2].data_ptr(), pinned[3].data_ptr(), v.n, p, q,
-                                  C.byref(c), C.byref(r)))
+        _abi.check(L.bc_count(pinned[0].data_ptr(), pinned[1].data_ptr(), u.n,
+                              pinned[2].data_ptr(), pinned[3].data_ptr(), v.n, p, q,
+                              C.byref(c), C.byref(r)))
         e2e_s, h2d, d2h = [], 0, 0
         for _ in range(args.steps):
             torch.cuda.synchronize()
@@ -378,18 +457,11 @@ def main():
 
     if rank == 0:
         peak, peak_src = measured_peak()
-        b_search = b_enum - b_l1  # the enumeration kernels' share of B_enum
-        achieved = b_search / t_enum / 1e9 if t_enum > 0 else None
         work = f"{CONFIG_DESC[args.config]} ({p},{q})"
-        tr = traffic_for(work)
-        physical = None
-        if tr and t_enum > 0:
-            physical = {
-                "dram_bytes": tr["dram_bytes"], "l2_bytes": tr["l2_bytes"],
-                "dram_gbs": tr["dram_bytes"] / t_enum / 1e9,
-                "dram_frac": tr["dram_bytes"] / t_enum / 1e9 / peak,
-                "l2_gbs": tr["l2_bytes"] / t_enum / 1e9,
-                "source": tr.get("source", "profiles/traffic.json")}
+        tr, tr_src = traffic_for(work) if world == 1 else (None, "captured at N = 1 only")
+        b_search = b_enum - b_l1  # the enumeration kernels' share of B_enum
+        dram = tr["dram_bytes"] if tr else None
+        achieved = dram / t_enum / 1e9 if dram and t_enum > 0 else None
         line = {
             "metric": METRIC, "value": total / (ms / 1e3), "unit": "bicliques/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -398,29 +470,40 @@ def main():
             "config": {"workload": work, "config": args.config, "p": p, "q": q,
                        "anchor": "UV"[instr.anchor], "tasks": instr.tasks_emitted,
                        "parallelism": f"root-shard{world}" + ("+2hop-shard" if world > 1 else ""),
+                       "dist_backend": args.dist_backend if world > 1 else None,
+                       "count_check": "equals tests/golden" if want is not None else "oracle in tests",
                        "l2": "flushed between timed steps (256 MiB device write)"},
             "phases_ms": {"prep": 1e3 * statistics.mean(prep_s),
                           "level1": 1e3 * statistics.mean(level1_s),
                           "enum": 1e3 * statistics.mean(enum_s)},
-            "roofline": {"bound": "hbm",
-                         "kernel": "enumeration kernels of one step (enum_kernel; on deep "
-                                   "searches its triage/split launches + sub_kernel)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if achieved else None,
-                         "traffic": tr["dram_bytes"] if tr else None,
-                         "algorithmic_bytes": b_search,
-                         "algorithmic": "B_enum (SURVEY 8(d)) minus its level-1 part: 8 B x "
-                                        "sum(|a|+|b|) HTB words over the reference's "
-                                        "intersections below level 1, tallied on device "
-                                        "(== oracle); the kernels re-index candidates into "
-                                        "task-local bitsets, so they move far fewer physical "
-                                        "bytes (SURVEY 8(d) rule 3): read `physical`",
-                         "per_unit_bytes": b_search / max(instr.tasks_emitted, 1),
-                         "units": f"{instr.tasks_emitted} (root, second) tasks",
-                         "launch_ms": 1e3 * t_enum, "share_of_step": t_enum / (ms / 1e3),
-                         "physical": physical, "b_enum_total_bytes": b_enum,
-                         "b_min_bytes": b_min, "peak_source": peak_src},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "enumeration kernels of one step (filter_kernel, enum_kernel "
+                          "triage/split/whole-task launches, sub_kernel), the dominant phase",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None,
+                "traffic": dram,
+                "achieved_is": "DRAM bytes of those kernels per step (ncu capture of this "
+                               "build) / their in-run CUDA-event time",
+                "traffic_source": tr_src,
+                "algorithmic_bytes": comp,
+                "algorithmic": "compulsory bytes: every input the enumeration kernels read, "
+                               "once (level-1 facts, queue, C_R1 lists, opposite-layer CSR, "
+                               "dir2 HTB); traffic / algorithmic = re-read factor",
+                "algorithmic_frac": comp / t_enum / 1e9 / peak if t_enum > 0 else None,
+                "l2_bytes": tr["l2_bytes"] if tr else None,
+                "l2_gbs": tr["l2_bytes"] / t_enum / 1e9 if tr and t_enum > 0 else None,
+                "merge_equiv_bytes": b_search,
+                "merge_equiv_gbs": b_search / t_enum / 1e9 if t_enum > 0 else None,
+                "merge_equiv": "B_enum (SURVEY 8(d)) below level 1: 8 B x sum(|a|+|b|) HTB "
+                               "words over the reference's intersections (device tally == "
+                               "oracle); the kernels re-index into task-local bitsets and "
+                               "never move these bytes",
+                "b_enum_total_bytes": b_enum, "b_min_bytes": b_min,
+                "launch_ms": 1e3 * t_enum, "share_of_step": t_enum / (ms / 1e3),
+                "units": f"{instr.tasks_emitted} (root, second) tasks",
+                "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     dg.close()

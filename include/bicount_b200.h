@@ -112,6 +112,8 @@ typedef struct bc_report {
   double time_total;             /* s: whole call */
   int64_t level1_operand_words;  /* BC_FLAG_INSTRUMENT: the level-1 share of operand_words */
   int64_t nesting_checked;       /* BC_FLAG_CHECK_NESTING: child C_L ids checked */
+  int64_t level1_entries;        /* C_R1 list entries written by the wedge-scatter level 1
+                                    (0 on the probe path): the level-1 lists' size / 4 B */
 } bc_report;
 
 /* Export ids for bc_export (device structures, for parity tests). */

@@ -55,7 +55,8 @@ class BcReport(C.Structure):
                 ("d2h_bytes", C.c_int64), ("time_h2d", C.c_double),
                 ("time_prep", C.c_double), ("time_level1", C.c_double),
                 ("time_enum", C.c_double), ("time_total", C.c_double),
-                ("level1_operand_words", C.c_int64), ("nesting_checked", C.c_int64)]
+                ("level1_operand_words", C.c_int64), ("nesting_checked", C.c_int64),
+                ("level1_entries", C.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

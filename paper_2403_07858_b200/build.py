@@ -17,6 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbicount_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+         "--expt-relaxed-constexpr"]
 
 
 def nvcc() -> str:
@@ -35,6 +37,19 @@ def deps() -> list[str]:
         os.path.join(HERE, "..", "include", "bicount_b200.h")]
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) of every build input and the nvcc flags: the key under which ncu
+    captures of this build are filed (profiles/r2/traffic.json)."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    for d in sorted(deps(), key=os.path.basename):
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
@@ -48,8 +63,7 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     if not force and out is None and up_to_date():
         return LIB
     # one nvcc per translation unit in parallel, then one link
-    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-             "--expt-relaxed-constexpr", *(extra or [])]
+    flags = [*FLAGS, *(extra or [])]
     if verbose:
         flags.insert(0, "-Xptxas=-v")
     tag = os.path.basename(lib).replace(".so", "")

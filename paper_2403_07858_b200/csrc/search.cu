@@ -862,7 +862,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   BC_CUDA(cudaEventCreate(&e1));
   BC_CUDA(cudaEventCreate(&e2));
   BC_CUDA(cudaEventRecord(e0, st));
-  int64_t n_alive = 0, n_split = 0, n_sub_total = 0;
+  int64_t n_alive = 0, n_split = 0, n_sub_total = 0, l1_entries = 0;
   if (nloc > 0 && s.p_eff == 1) {
     p1_kernel<<<sms * 8, 256, 0, st>>>(P, s.aoff);
     BC_CHECK_LAUNCH();
@@ -988,6 +988,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       copy_d2h(&n_entries, l1_roff.p + nloc, sizeof n_entries, st);
       BC_CUDA(cudaStreamSynchronize(st));
       l1_lists.alloc(n_entries, st);
+      l1_entries = n_entries;
       l1_cursors<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
           s.tasks.p, ltask.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p,
           s.dir_off.p, l1_roff.p, aux.p);
@@ -1457,6 +1458,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   out.overflow = h_ovf ? 1 : 0;
   out.tasks_consumed = (int64_t)h_ctr[CTR_CONSUMED];
   out.nesting_checked = (int64_t)h_ctr[CTR_NEST_CHECKED];
+  out.level1_entries = l1_entries;
   out.tasks_alive = n_alive;
   out.tasks_split = n_split;
   out.tasks_stolen = (int64_t)h_ctr[CTR_STOLEN];

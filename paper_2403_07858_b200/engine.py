@@ -526,6 +526,8 @@ def allreduce_count(partial: int, group=None, device=None) -> int:
     import torch
     import torch.distributed as dist
 
+    if dist.get_backend(group) == "gloo":
+        device = None  # gloo reduces host tensors (CPU tests, one-GPU multi-rank runs)
     t = torch.tensor(split_limbs(partial), dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return merge_limbs(t.cpu().tolist())

@@ -278,13 +278,30 @@ def graph_from_torch_csr(u_off, u_idx, v_off, v_idx) -> BipartiteGraph:
                                    v_off.cpu().numpy(), v_idx.cpu().numpy())
 
 
+# C5H: C5's base graph with many more planted core triples, so the (8,8) search -- not
+# the level-1 pass -- dominates and one GPU runs for seconds: the multi-GPU scaling
+# workload; calibrated on a B200
+C5H_CORES, C5H_CORE_SEED = 1024, 11
+
+DEVICE_CONFIGS = {
+    "C5": {},
+    "C5H": {"n_cores": C5H_CORES, "core_seed": C5H_CORE_SEED},
+}
+
+
+def build_device_config(name: str, device: str = "cuda"):
+    """(u_off, u_idx, v_off, v_idx) torch tensors of a device-generated config."""
+    return fr_shaped_csr(device=device, **DEVICE_CONFIGS[name])
+
+
 CONFIGS = {
     # name: (builder, [(p, q), ...])
     "C1": (lambda: erdos_renyi(2000, 2000, 20000, 1), [(2, 2)]),
     "C2": (lambda: chung_lu(100000, 50000, 1000000, 2.5, 7, 1.15), [(4, 4)]),
     "C3": (lambda: chung_lu(56519, 120867, 440237, 2.5, 11, 1.3), [(3, 6), (6, 3)]),
     "C4": (planted_dense, [(8, 8)]),
-    "C5": (lambda: graph_from_torch_csr(*fr_shaped_csr(device=_gen_device())), [(8, 8)]),
+    "C5": (lambda: graph_from_torch_csr(*build_device_config("C5", _gen_device())), [(8, 8)]),
+    "C5H": (lambda: graph_from_torch_csr(*build_device_config("C5H", _gen_device())), [(8, 8)]),
 }
 
 

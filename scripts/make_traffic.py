@@ -1,5 +1,7 @@
-"""profiles/traffic.json from ncu launch lists: DRAM and L2 bytes of the enumeration
-kernels (enum_kernel, sub_kernel) of one count, keyed by the bench workload string.
+"""profiles/r2/traffic.json from ncu launch lists: DRAM and L2 bytes of the enumeration
+kernels (filter_kernel, enum_kernel, sub_kernel) of one count, keyed by the bench workload
+string and stamped with the source hash of the build that was captured (bench.py uses an
+entry only for that build).  Run it on the launch list of the current tree.
 
     python scripts/make_traffic.py '<workload>' <launches.csv> [<workload> <csv> ...]
 """
@@ -9,7 +11,10 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-out_path = os.path.join(ROOT, "profiles", "traffic.json")
+sys.path.insert(0, ROOT)
+from paper_2403_07858_b200 import build  # noqa: E402
+
+out_path = os.path.join(ROOT, "profiles", "r2", "traffic.json")
 try:
     out = json.load(open(out_path))
 except (OSError, ValueError):
@@ -29,6 +34,7 @@ for work, path in zip(args[::2], args[1::2]):
     l2 = sum(m.get("lts__t_bytes.sum", 0) for m in per.values())
     ms = sum(m.get("gpu__time_duration.sum", 0) for m in per.values()) / 1e6
     out[work] = {"dram_bytes": int(dram), "l2_bytes": int(l2), "ncu_ms": round(ms, 3),
-                 "launches": len(per), "source": os.path.relpath(path, ROOT)}
+                 "launches": len(per), "source": os.path.relpath(path, ROOT),
+                 "src_sha": build.source_hash()}
     print(work, out[work])
 json.dump(out, open(out_path, "w"), indent=1)

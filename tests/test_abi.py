@@ -42,8 +42,8 @@ def test_abi_version_and_device_probe(lib):
 def test_struct_layout_matches_header():
     # bc_config: 8 x int32, then ptr/int64 pairs x 4 -> 32 + 64 = 96 bytes
     assert C.sizeof(_abi.BcConfig) == 96
-    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 + 2 i64 = 16 + 16 + 144 + 40 + 16
-    assert C.sizeof(_abi.BcReport) == 232
+    # bc_report: 2 u64 + 4 i32 + 18 i64 + 5 f64 + 3 i64 = 16 + 16 + 144 + 40 + 24
+    assert C.sizeof(_abi.BcReport) == 240
     # and the C compiler agrees with ctypes on every field offset
     import subprocess
     import tempfile

@@ -32,10 +32,11 @@ def test_nesting_assert_mode_runs_clean():
     rep = count_bicliques(g, 4, 2, EngineConfig(check_nesting=True))
     assert rep.count == O.brute_force_count(g, 4, 2)
     for seed in (3, 4, 5):
-        g = synth.random_bipartite(40, 36, 0.35, seed)
-        rep = count_bicliques(g, 5, 3, EngineConfig(check_nesting=True))
-        assert rep.count == O.count(g, 5, 3).count
-        assert rep.device["nesting_checked"] > 0
+        g = synth.random_bipartite(40, 36, 0.5, seed)
+        for anchor in ("U", "V"):  # p_eff 5 / 4: both descend below level 2
+            rep = count_bicliques(g, 5, 4, EngineConfig(check_nesting=True, anchor=anchor))
+            assert rep.count == O.count(g, 5, 4, anchor=anchor).count > 0
+            assert rep.device["nesting_checked"] > 0
 
 
 def test_workers_agree_and_tally_exactly_once():
