@@ -32,7 +32,7 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, scenario, q):
+def _worker(rank, world, port, scenario, outq):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -75,21 +75,22 @@ def _worker(rank, world, port, scenario, q):
                 parts = P.budgeted_partition(g, idx, int(w.sum() // 4))
             total, local = P.count_partitioned_distributed(g, parts, 3, 6, rank=rank, world=world)
             out["C3|partitioned"] = (str(total), local.tasks_consumed, parts.group_count)
-        q.put((rank, out))
+        outq.put((rank, out))
     finally:
         dist.destroy_process_group()
 
 
 def _run(world, scenario):
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    outq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, scenario, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, scenario, outq))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
     for _ in procs:
-        r, out = q.get()
+        r, out = outq.get(timeout=600)  # a rank that died raises queue.Empty, not a hang
         res[r] = out
     for p in procs:
         p.join(timeout=600)
