@@ -87,6 +87,8 @@ typedef struct bc_config {
                                    C_L = C_L1 & dir2(u) from the HTB arenas and check each id
                                    against the root's directed 2-hop list; BC_EASSERT on a
                                    violation */
+#define BC_FLAG_FULL_ROWS 1024  /* wedge-scatter frames walk whole opposite-layer rows N(v)
+                                   instead of the root-restricted rows N(v) & dir2(r) (tests) */
 
 /* CountReport (engine.py:64-79) plus device measurements. */
 typedef struct bc_report {

@@ -269,7 +269,18 @@ __global__ void __launch_bounds__(256) nesting_check(Params P, const Info *__res
 // counts hits per (unit, slot); a column scan turns them into per-task list
 // offsets and per-unit cursors; pass 2 appends, ranking the same-slot hits of a
 // round by lane (__match_any_sync) so every list comes out sorted.
+//
+// The same walk also yields the root-restricted rows R(r, v) = N(v) & dir2(r): every
+// later wedge walk of a task (r, s) (the survivor counts and candidate rows of
+// build_frame_R) only looks for x in C_L1 = dir2(r) & dir2(s), so it can walk R(r, v)
+// instead of the whole row N(v) (C5: 4.0e9 instead of 1.7e10 wedges).  Per-edge
+// cursors live in shared memory (one per lane's edge of the current 32-edge round);
+// a row's order is free, so hits take their places by shared-memory atomics.
 // ---------------------------------------------------------------------------
+struct U32ToI64 {
+  __host__ __device__ __forceinline__ int64_t operator()(uint32_t x) const { return (int64_t)x; }
+};
+
 constexpr int L1_CH = 1024;
 constexpr int L1_THREADS = 128;
 
@@ -290,6 +301,14 @@ struct L1Args {
   int shard, nshards;
   int32_t *lists;           // pass 2
   unsigned long long *next;
+  // root-restricted rows R(r, v) = N(v) & dir2(r) for every edge e = (r, v) of a unit
+  // (null: not built).  Pass 1 counts |R(r, v)| into rcnt[e]; pass 2 writes the rows
+  // at roffE[e] (ascending ids) and, beside each C_R1 list entry v of task (r, s), the
+  // entry's row {roffE[e], |R(r, v)|} in lseg
+  uint32_t *rcnt;
+  const int64_t *__restrict__ roffE;
+  int32_t *rrows;
+  uint2 *lseg;
 };
 
 struct RootMap {
@@ -336,8 +355,11 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int mw = A.map_words;
-  uint32_t *bits = mw ? sm + (int64_t)wib * (mw + (mw + 1) / 2) : nullptr;
+  uint32_t *wsm = sm + (int64_t)wib * (mw + (mw + 1) / 2 + 32);
+  uint32_t *bits = mw ? wsm : nullptr;
   uint16_t *pre = mw ? (uint16_t *)(bits + mw) : nullptr;
+  uint32_t *runs = wsm + mw + (mw + 1) / 2;  // R(r, v) cursor of the round's edge base + lane
+  const bool rr = A.rcnt != nullptr;
   if (bits)
     for (int i = lane; i < mw; i += 32) bits[i] = 0;
   __syncwarp();
@@ -362,11 +384,18 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
       int32_t v = 0;
       int64_t st = 0;
       int len = 0;
+      uint32_t rs = 0, rl = 0;  // this lane's edge: R(r, v) start and length (pass 2)
       if (e < e1) {
         v = __ldg(A.aidx + e);
         st = __ldg(A.boff + v);
         len = (int)(__ldg(A.boff + v + 1) - st);
+        if (rr && FILL) {
+          rs = (uint32_t)A.roffE[e];
+          rl = (uint32_t)(A.roffE[e + 1] - A.roffE[e]);
+        }
       }
+      if (rr) runs[lane] = rs;
+      __syncwarp();
       int incl = len;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -377,8 +406,9 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
       const int T = __shfl_sync(FULL, incl, 31);
       constexpr int U = 4;  // gathers in flight per lane
       for (int r0 = 0; r0 < T; r0 += 32 * U) {
-        int ks[U];
+        int ks[U], os[U];
         int32_t vs[U];
+        uint32_t rss[U], rls[U];
 #pragma unroll
         for (int uu = 0; uu < U; uu++) {
           const int pos = r0 + 32 * uu + lane;
@@ -392,12 +422,24 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
           const int64_t so = __shfl_sync(FULL, st, sl);
           const int eo = __shfl_sync(FULL, excl, sl);
           vs[uu] = __shfl_sync(FULL, v, sl);
+          os[uu] = sl;
+          if (FILL && rr) {
+            rss[uu] = __shfl_sync(FULL, rs, sl);
+            rls[uu] = __shfl_sync(FULL, rl, sl);
+          }
           ks[uu] = pos < T ? __ldg(A.bidx + so + (pos - eo)) : -1;
         }
 #pragma unroll
         for (int uu = 0; uu < U; uu++) {
-          int k = ks[uu] >= 0 ? m.slot(ks[uu]) : -1;
+          const int kd = ks[uu] >= 0 ? m.slot(ks[uu]) : -1;  // s in dir2(r)
+          int k = kd;
           if (k >= 0 && (T0 + k) % A.nshards != A.shard) k = -1;
+          // R(r, v) of every local edge holds all of dir2(r), whatever the shard; its order
+          // is free (the walks only count), so a shared-memory atomic places each hit
+          if (rr && kd >= 0) {
+            const uint32_t at = atomicAdd(runs + os[uu], 1u);
+            if (FILL) A.rrows[at] = ks[uu];
+          }
           if (!FILL) {
             if (k >= 0) atomicAdd(col + k, 1ull);
           } else {
@@ -406,13 +448,18 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
             const unsigned long long c0 = k >= 0 ? col[k] : 0ull;
             __syncwarp();
             if (k >= 0) {
-              A.lists[c0 + __popc(grp & lanemask_lt())] = vs[uu];
+              const unsigned long long at = c0 + __popc(grp & lanemask_lt());
+              A.lists[at] = vs[uu];
+              if (rr) A.lseg[at] = make_uint2(rss[uu], rls[uu]);
               if (((grp >> lane) >> 1) == 0) col[k] = c0 + __popc(grp);
             }
             __syncwarp();
           }
         }
       }
+      __syncwarp();
+      if (rr && !FILL && e < e1) A.rcnt[e] = runs[lane];
+      __syncwarp();
     }
     __syncwarp();  // lanes still probing the map must finish before it is cleared
     rootmap_set(m, false);
@@ -552,8 +599,8 @@ __global__ void l1_pool(const int64_t *__restrict__ aoff, const int32_t *__restr
 // members' degrees (wedge scatter) vs 2 * |C_L1| * words(C_R1) (probes)
 __global__ void rows_cost(const Info *__restrict__ info, int64_t nloc, int stride,
                           const int64_t *__restrict__ roff, const int32_t *__restrict__ lists,
-                          const int64_t *__restrict__ boff, int p_eff, int q,
-                          unsigned long long *out) {
+                          const int64_t *__restrict__ boff, const uint2 *__restrict__ lseg,
+                          int p_eff, int q, unsigned long long *out) {
   const int lane = lane_id();
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -562,8 +609,12 @@ __global__ void rows_cost(const Info *__restrict__ info, int64_t nloc, int strid
     const Info in = info[j];
     if (in.cr < q || in.cl < p_eff - 2) continue;
     for (int64_t i = roff[j] + lane; i < roff[j + 1]; i += 32) {
-      const int v = lists[i];
-      sc += (unsigned long long)(boff[v + 1] - boff[v]);
+      if (lseg) {  // the walk reads the root-restricted row R(r, v)
+        sc += lseg[i].y;
+      } else {
+        const int v = lists[i];
+        sc += (unsigned long long)(boff[v + 1] - boff[v]);
+      }
     }
     if (lane == 0) pr += 2ull * (unsigned long long)in.cl * (unsigned long long)in.wr;
   }
@@ -849,6 +900,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.claims = want_claims ? claims.p : nullptr;
   P.roff = nullptr;
   P.lists = nullptr;
+  P.lseg = nullptr;
+  P.rrows = nullptr;
   P.rowR_mode = (cfg.flags & BC_FLAG_ROWR_SCATTER) ? 1 : (cfg.flags & BC_FLAG_ROWR_PROBE) ? 2 : 0;
   if (P.rowR_mode == 0) P.rowR_mode = env_int("BC_ROWS_MODE", 0);  // development A/B
   // slot map over anchor words for rowL (u16 per word) when it is small
@@ -877,6 +930,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     // 2-hop pools cost less than the per-task probes of the shorter adjacency slice
     DBuf<int64_t> l1_roff;
     DBuf<int32_t> l1_lists;
+    DBuf<uint32_t> rr_cnt;  // root-restricted rows (l1_scatter)
+    DBuf<int64_t> rr_off;
+    DBuf<int32_t> rr_rows;
+    DBuf<uint2> rr_seg;
     int l1_mode = (cfg.flags & BC_FLAG_L1_SCATTER) ? 1 : (cfg.flags & BC_FLAG_L1_PROBE) ? 2 : 0;
     if (l1_mode == 0) l1_mode = env_int("BC_L1_MODE", 0);  // development A/B
     if (l1_mode == 0) {
@@ -950,8 +1007,19 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       A1.shard = owner.p ? 0 : shard;  // root sharding: every slot of an owned root is local
       A1.nshards = owner.p ? 1 : nshards;
       A1.next = nxt.p;
+      // root-restricted rows for the compact frames' wedge walks (slot map needed, p_eff >= 4)
+      const bool want_rr = s.p_eff >= 4 && (s.n + 31) / 32 <= 4096 &&
+                           !(cfg.flags & BC_FLAG_FULL_ROWS);
+      int64_t n_anchor_edges = 0;
+      if (want_rr) {
+        copy_d2h(&n_anchor_edges, s.aoff + n, sizeof n_anchor_edges, st);
+        BC_CUDA(cudaStreamSynchronize(st));
+        rr_cnt.alloc(n_anchor_edges, st);
+        rr_cnt.zero();
+        A1.rcnt = rr_cnt.p;
+      }
       const int l1w = L1_THREADS / 32;
-      const size_t l1smem = (size_t)l1w * (A1.map_words + (A1.map_words + 1) / 2) * 4;
+      const size_t l1smem = (size_t)l1w * (A1.map_words + (A1.map_words + 1) / 2 + 32) * 4;
       int per_sm = 0;
       BC_CUDA(cudaFuncSetAttribute(l1_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)l1smem));
@@ -989,6 +1057,34 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       BC_CUDA(cudaStreamSynchronize(st));
       l1_lists.alloc(n_entries, st);
       l1_entries = n_entries;
+      if (A1.rcnt) {
+        // restricted-row offsets; the per-entry row starts are u32 (else: whole rows)
+        const int64_t E = n_anchor_edges;
+        rr_off.alloc(E + 1, st);
+        U32ToI64 cv;
+        cub::TransformInputIterator<int64_t, U32ToI64, const uint32_t *> it(rr_cnt.p, cv);
+        size_t tmp = 0;
+        BC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, it, rr_off.p + 1, E, st));
+        DBuf<char> tb;
+        tb.alloc(tmp, st);
+        BC_CUDA(cub::DeviceScan::InclusiveSum(tb.p, tmp, it, rr_off.p + 1, E, st));
+        BC_CUDA(cudaMemsetAsync(rr_off.p, 0, sizeof(int64_t), st));
+        int64_t rr_total = 0;
+        copy_d2h(&rr_total, rr_off.p + E, sizeof rr_total, st);
+        BC_CUDA(cudaStreamSynchronize(st));
+        launches += 2;
+        if (rr_total < (int64_t(1) << 32)) {
+          rr_rows.alloc(rr_total, st);
+          rr_seg.alloc(n_entries, st);
+          A1.roffE = rr_off.p;
+          A1.rrows = rr_rows.p;
+          A1.lseg = rr_seg.p;
+          if (getenv("BC_DEBUG"))
+            fprintf(stderr, "[bc level1] restricted rows: %lld entries\n", (long long)rr_total);
+        } else {
+          A1.rcnt = nullptr;
+        }
+      }
       l1_cursors<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
           s.tasks.p, ltask.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p,
           s.dir_off.p, l1_roff.p, aux.p);
@@ -1001,6 +1097,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       launches += 12;
       P.roff = l1_roff.p;
       P.lists = l1_lists.p;
+      if (A1.rcnt) {
+        P.lseg = rr_seg.p;
+        P.rrows = rr_rows.p;
+      }
       if (getenv("BC_DEBUG")) {
         BC_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr, "[bc level1] scatter: %d units, %lld aux, %lld C_R1 entries\n", n_units,
@@ -1115,8 +1215,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             rc.zero();
             const int stride = nloc > (int64_t(1) << 20) ? 16 : 1;
             rows_cost<<<(unsigned)std::min<int64_t>((nloc / stride * 32 + 255) / 256 + 1, sms * 16), 256,
-                        0, st>>>(info.p, nloc, stride, P.roff, P.lists, s.boff, s.p_eff, s.q_eff,
-                                 rc.p);
+                        0, st>>>(info.p, nloc, stride, P.roff, P.lists, s.boff, P.lseg, s.p_eff,
+                                 s.q_eff, rc.p);
             unsigned long long hc[2];
             copy_d2h(hc, rc.p, sizeof hc, st);
             BC_CUDA(cudaStreamSynchronize(st));
@@ -1242,7 +1342,16 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               EnumArgs F = B;
               F.heavy = medium.p;
               F.heavy_ns1 = medium_ns1.p;
-              if (B.gscratch && fblocks > blocks) F.gscratch = nullptr;  // (sized for `blocks`)
+              // the filter's frames are the first half only (C_R1, C_L1, ids, counters);
+              // its own per-warp scratch when it runs more warps than the triage kernel
+              DBuf<uint32_t> fgs;
+              if (B.gscratch && fblocks > blocks) {
+                const int64_t w = (max_ro + 31) & ~int64_t(31);
+                const int64_t cap_w = ((int64_t(1) << 30) / (fblocks * wpb)) & ~int64_t(31);
+                F.gscratch_words = std::min(w, cap_w);
+                fgs.alloc((size_t)fblocks * wpb * F.gscratch_words, st);
+                F.gscratch = fgs.p;
+              }
               BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
               BC_CUDA(cudaMemsetAsync(ctr.p + CTR_HEAVY, 0, 8, st));
               dt.mark("pre-filter");
@@ -1252,9 +1361,23 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               unsigned long long hm = 0;
               copy_d2h(&hm, ctr.p + CTR_HEAVY, sizeof hm, st);
               BC_CUDA(cudaStreamSynchronize(st));
+              // back to emission order (the filter pushes in completion order): a root's
+              // tasks stay adjacent, so the triage kernel re-reads their rows from L2
+              DBuf<int32_t> msorted;
+              msorted.alloc(hm, st);
+              {
+                size_t tmp = 0;
+                BC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, medium.p, msorted.p,
+                                                       (int64_t)hm, 0, 32, st));
+                DBuf<char> tb;
+                tb.alloc(tmp, st);
+                BC_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, tmp, medium.p, msorted.p,
+                                                       (int64_t)hm, 0, 32, st));
+              }
+              medium = std::move(msorted);
               B.queue = medium.p;
               B.q1 = (int64_t)hm;
-              launches++;
+              launches += 2;
               if (dt.on) fprintf(stderr, "[bc search] medium %llu\n", hm);
             }
             BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));

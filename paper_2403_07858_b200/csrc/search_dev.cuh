@@ -87,6 +87,11 @@ struct Params {
   const int64_t *__restrict__ ltask;    // root sharding: global id of local task j (or null:
                                         //   task interleave t = shard + j * nshards)
   unsigned *claims;                     // optional [n_tasks]: claims per task (track_tasks)
+  // root-restricted rows (wedge-scatter level 1): C_R1 list entry i of task (r, s) holds
+  // member v = lists[i] and lseg[i] = {start, len} of R(r, v) = N(v) & dir2(r) in rrows
+  // (or null: the wedge walks read the whole rows N(v))
+  const uint2 *__restrict__ lseg;
+  const int32_t *__restrict__ rrows;
 };
 
 // global task id of this shard's local task j
@@ -1102,18 +1107,30 @@ __device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int 
 // concatenated rows, so every lane issues a load per step however short the
 // rows are.  Work is sum_{v in C_R1} deg(v), read as contiguous rows, instead
 // of |C_L1| probes of (possibly hub-sized) adjacency rows.
+//
+// With root-restricted rows (P.lseg), member i's row is R(r, v) = N(v) & dir2(r)
+// (list entry lbase + i): every x of C_L1 = dir2(r) & dir2(s) in N(v) is in it, so the
+// hits are the same and the walk is shorter.
 template <typename F>
 __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f, const Dims &d,
-                                                const int *members, const uint16_t *map, F fn) {
+                                                const int *members, const uint16_t *map,
+                                                int64_t lbase, F fn) {
   const int lane = lane_id();
+  const int32_t *__restrict__ src = P.lseg ? P.rrows : P.g.bidx;
   for (int b0 = 0; b0 < d.nR; b0 += 32) {
     const int i = b0 + lane;
     int64_t start = 0;
     int len = 0;
     if (i < d.nR) {
-      const int v = members[i];
-      start = __ldg(P.g.boff + v);
-      len = (int)(__ldg(P.g.boff + v + 1) - start);
+      if (P.lseg) {
+        const uint2 sg = __ldg(P.lseg + lbase + i);
+        start = sg.x;
+        len = (int)sg.y;
+      } else {
+        const int v = members[i];
+        start = __ldg(P.g.boff + v);
+        len = (int)(__ldg(P.g.boff + v + 1) - start);
+      }
     }
     int incl = len;
 #pragma unroll
@@ -1139,7 +1156,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
         const int64_t st = __shfl_sync(FULL, start, sl);
         const int ex = __shfl_sync(FULL, excl, sl);
         own[u] = sl;
-        xs[u] = pos < T ? __ldg(P.g.bidx + st + (pos - ex)) : -1;
+        xs[u] = pos < T ? __ldg(src + st + (pos - ex)) : -1;
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -1204,7 +1221,8 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     for (int x = lane; x < d.nL; x += 32) f.lslot[x] = 0;
     __syncwarp();
     int *cnt = f.lslot;
-    for_member_hits(P, f, d, f.rids, map, [&](int, int lx) { atomicAdd(cnt + lx, 1); });
+    const int64_t lbase = P.lseg ? P.roff[j] : 0;
+    for_member_hits(P, f, d, f.rids, map, lbase, [&](int, int lx) { atomicAdd(cnt + lx, 1); });
     int base = 0;
     for (int x0 = 0; x0 < d.nL; x0 += 32) {
       const int x = x0 + lane;
@@ -1222,7 +1240,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
       uint32_t *rowR = f.rowR;
       const int *lslot = f.lslot;
       const int WR = d.WR;
-      for_member_hits(P, f, d, f.rids, map, [&](int i, int lx) {
+      for_member_hits(P, f, d, f.rids, map, lbase, [&](int i, int lx) {
         const int sl = lslot[lx];
         if (sl >= 0) atomicOr(rowR + (int64_t)sl * WR + (i >> 5), 1u << (i & 31));
       });
@@ -1599,7 +1617,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
 // the others go to `heavy` (the medium list) for the triage kernel.  Kept separate
 // so this kernel, which sees every task, stays small in instruction cache.
 #ifndef FILTER_MIN_BLOCKS
-#define FILTER_MIN_BLOCKS 3
+#define FILTER_MIN_BLOCKS 4
 #endif
 template <bool COMPACT>
 __global__ void __launch_bounds__(ENUM_THREADS, FILTER_MIN_BLOCKS) filter_kernel(Params P, EnumArgs A) {

@@ -47,6 +47,7 @@ class EngineConfig:
     instrument: bool = False  # tally reference-equivalent intersections (B_enum)
     level1: str = "auto"      # "scatter" (root-grouped wedge walk) | "probe" (per-task HTB)
     rows: str = "auto"        # candidate rows: "scatter" | "probe"
+    restricted_rows: bool = True  # scatter walks read N(v) & dir2(root), not all of N(v)
     shard_mode: str = "root"  # multi-GPU: whole roots, degree-balanced | "task" interleave
 
     def validate(self) -> None:
@@ -160,6 +161,8 @@ def _make_config(cfg: EngineConfig, anchor: str, rank, roots, shard=(0, 1), flag
     c.flags |= {"auto": 0, "scatter": _abi.BC_FLAG_L1_SCATTER, "probe": _abi.BC_FLAG_L1_PROBE}[cfg.level1]
     c.flags |= {"auto": 0, "scatter": _abi.BC_FLAG_ROWR_SCATTER,
                 "probe": _abi.BC_FLAG_ROWR_PROBE}[cfg.rows]
+    if not cfg.restricted_rows:
+        c.flags |= _abi.BC_FLAG_FULL_ROWS
     if cfg.shard_mode == "task":
         c.flags |= _abi.BC_FLAG_TASK_SHARD
     keep = []
