@@ -6,6 +6,16 @@
 #pragma once
 #include <climits>
 
+// Loops over task-local words and lists run a handful of iterations (C_R1 / C_L1 are a
+// few words): compiler unrolling only multiplies the code of kernels whose hot set
+// already exceeds the instruction cache (ncu: no_instruction was 65% of C5 sub_kernel's
+// stall samples), so loops are kept rolled unless marked otherwise.
+#ifndef BC_UNROLL_DEFAULT
+#define BC_LOOP _Pragma("unroll 1")
+#else
+#define BC_LOOP
+#endif
+
 #include "engine.h"
 
 namespace bc {
@@ -27,6 +37,7 @@ struct PhaseClock {
   unsigned long long t[8];
   long long last;
   __device__ __forceinline__ PhaseClock() : last(clk()) {
+    BC_LOOP
     for (int i = 0; i < 8; i++) t[i] = 0;
   }
   __device__ __forceinline__ void mark(int i) {
@@ -36,6 +47,7 @@ struct PhaseClock {
   }
   __device__ __forceinline__ void flush() {
     if ((threadIdx.x & 31) == 0)
+      BC_LOOP
       for (int i = 0; i < 8; i++) atomicAdd(&g_phase[i], t[i]);
   }
 };
@@ -150,6 +162,7 @@ __device__ __forceinline__ int warp_isect(const uint32_t *__restrict__ idx,
   const int lane = lane_id();
   int pos = 0, run = 0;
   int64_t lo = b0;
+  BC_LOOP
   for (int64_t base = a0; base < a1; base += 32) {
     const int64_t i = base + lane;
     int64_t j = b1;
@@ -353,6 +366,7 @@ __device__ __forceinline__ const uint32_t *rowL_of(const Frame &f, const Dims &d
 __device__ __forceinline__ int lid_of(const Frame &f, const Dims &d, int x) {
   if (!f.compact) return f.lids[x];
   int lo = 0, hi = d.wL - 1;
+  BC_LOOP
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (f.l_pre[mid] <= x) lo = mid;
@@ -377,6 +391,7 @@ struct RowWriter {
   __device__ __forceinline__ RowWriter(uint32_t *r, int w) : row(r), W(w), cur(0), bits(0) {}
   __device__ __forceinline__ void flush_to(int w) {
     row[cur] = bits;
+    BC_LOOP
     for (int x = cur + 1; x < w; x++) row[x] = 0;
     cur = w;
     bits = 0;
@@ -402,6 +417,7 @@ struct RowWriter {
       set_run(pre, __popc(v));
       return;
     }
+    BC_LOOP
     while (m) {
       const int b = __ffs(m) - 1;
       m &= m - 1;
@@ -424,6 +440,7 @@ __device__ __forceinline__ void local_row(const uint32_t *s_idx, const uint32_t 
   RowWriter rw(row, W);
   if (dense_row) {
     int k = 0;
+    BC_LOOP
     for (; k + 4 <= ns; k += 4) {  // four independent probes in flight
       uint32_t d[4];
 #pragma unroll
@@ -434,12 +451,14 @@ __device__ __forceinline__ void local_row(const uint32_t *s_idx, const uint32_t 
         if (m) rw.add(s_pre[k + t], s_val[k + t], m);
       }
     }
+    BC_LOOP
     for (; k < ns; k++) {
       const uint32_t m = s_val[k] & __ldg(dense_row + s_idx[k]);
       if (m) rw.add(s_pre[k], s_val[k], m);
     }
   } else if (ns <= g1 - g0) {
     int64_t lo = g0;
+    BC_LOOP
     for (int k = 0; k < ns; k++) {
       const uint32_t key = s_idx[k];
       const int64_t j = lower_bound_u32(gidx, lo, g1, key);
@@ -454,9 +473,11 @@ __device__ __forceinline__ void local_row(const uint32_t *s_idx, const uint32_t 
     }
   } else {
     int lo = 0;
+    BC_LOOP
     for (int64_t j = g0; j < g1; j++) {
       const uint32_t key = __ldg(gidx + j);
       int a = lo, b = ns;
+      BC_LOOP
       while (a < b) {
         const int mid = (a + b) >> 1;
         if (s_idx[mid] < key) a = mid + 1;
@@ -481,6 +502,7 @@ __device__ __forceinline__ void local_row_map(const uint16_t *map, const uint32_
                                               const uint32_t *__restrict__ gval, int64_t g0,
                                               int64_t g1, uint32_t *row, int W) {
   RowWriter rw(row, W);
+  BC_LOOP
   for (int64_t j = g0; j < g1; j++) {
     const int k = map[__ldg(gidx + j)];
     if (k != 0xffff) {
@@ -500,6 +522,7 @@ __device__ __forceinline__ int words_touched(const uint32_t *set, const uint32_t
   const int lane = lane_id();
   int c = 0;
   unsigned long long cin_chunk = 0;
+  BC_LOOP
   for (int w0 = 0; w0 < W; w0 += 32) {
     const int w = w0 + lane;
     const uint32_t x = w < W ? set[w] : 0u, L = w < W ? last[w] : FULL;
@@ -523,6 +546,7 @@ __device__ __forceinline__ int lane_words(const uint32_t *R, const uint32_t *ru,
                                           const uint32_t *ru2 = nullptr) {
   int c = 0;
   unsigned long long carry = 0;
+  BC_LOOP
   for (int w = 0; w < W; w++) {
     const uint32_t x = R[w] & ru[w] & (ru2 ? ru2[w] : FULL), L = last[w];
     const unsigned long long sum = (unsigned long long)(x & ~L) + (unsigned long long)(~L) + carry;
@@ -536,9 +560,11 @@ __device__ __forceinline__ int lane_words(const uint32_t *R, const uint32_t *ru,
 __device__ __forceinline__ int compact_bits(const uint32_t *set, int W, int *cand) {
   const int lane = lane_id();
   int n = 0;
+  BC_LOOP
   for (int w0 = 0; w0 < W; w0 += 32) {
     const uint32_t mine = w0 + lane < W ? set[w0 + lane] : 0u;
     unsigned nz = __ballot_sync(FULL, mine != 0);
+    BC_LOOP
     while (nz) {
       const int x = __ffs(nz) - 1;
       nz &= nz - 1;
@@ -556,9 +582,11 @@ __device__ __forceinline__ int compact_bits_and(const uint32_t *set, const uint3
                                                 int *cand) {
   const int lane = lane_id();
   int n = 0;
+  BC_LOOP
   for (int w0 = 0; w0 < W; w0 += 32) {
     const uint32_t mine = w0 + lane < W ? set[w0 + lane] & filter[w0 + lane] : 0u;
     unsigned nz = __ballot_sync(FULL, mine != 0);
+    BC_LOOP
     while (nz) {
       const int x = __ffs(nz) - 1;
       nz &= nz - 1;
@@ -621,6 +649,7 @@ __device__ __forceinline__ void eval_leaves(const Params &P, const Frame &f, con
   const int excl = incl - cnt;
   const int total = __shfl_sync(FULL, incl, 31);
   const int WR = d.WR;
+  BC_LOOP
   for (int r0 = 0; r0 < total; r0 += 32) {
     const int k = r0 + lane;
     int o = 0;
@@ -650,6 +679,7 @@ __device__ __forceinline__ void eval_leaves(const Params &P, const Frame &f, con
             if (x < WR) c += __popc(pr[x] & rw[x]);
         } else {
           const uint32_t *ru = rowR_of(f, d, slot_u[so]);
+          BC_LOOP
           for (int x = 0; x < WR; x++) c += __popc(R[x] & ru[x] & rw[x]);
         }
       }
@@ -679,6 +709,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
   const int WR = d.WR, WL = d.WL;
   const uint32_t *R = f.setR + (level - 1) * WR;
   const uint32_t *Ls = f.setL + (level - 1) * WL;
+  BC_LOOP
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
     const bool act = i < n;
@@ -709,6 +740,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
       }
       const int excl = incl - len;
       const int T = __shfl_sync(FULL, incl, 31);
+      BC_LOOP
       for (int r0 = 0; r0 < T; r0 += 32) {
         const int pos = r0 + lane;
         // owning slot: the last lane whose exclusive offset is <= pos
@@ -741,6 +773,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
       int ncand = 0;
       const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL;
       const uint32_t *rl2 = act && list2 ? rowL_of(f, d, list2[i]) : nullptr;
+      BC_LOOP
       for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
         uint32_t m = 0;
         if (act && x < WL) m = Ls[x] & rl[x] & (rl2 ? rl2[x] : FULL);
@@ -777,6 +810,7 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
   const int *kids = f.surv + li * f.surv_cap;
   const int need_g = P.p_eff - level - 3;  // prune_keep at level + 2
   int work = 0, fill = 0;
+  BC_LOOP
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
     const bool act = i < n;
@@ -789,6 +823,7 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
     const int wr_u = act ? lane_words(R, ru, f.r_last, WR) : 0;
     const int wl_u = act ? lane_words(Ls, rl, f.l_last, WL) : 0;
     int ncand_u = 0;
+    BC_LOOP
     for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
       const uint32_t mall = act && x < WL ? Ls[x] & rl[x] : 0u;
       ncand_u += __popc(mall);
@@ -802,6 +837,7 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
       }
       const int excl = incl - cnt;
       const int total = __shfl_sync(FULL, incl, 31);
+      BC_LOOP
       for (int r0 = 0; r0 < total; r0 += 32) {
         const int k = r0 + lane;
         int o = 0;
@@ -843,6 +879,7 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
             }
             const uint32_t *rlo = rowL_of(f, d, uo), *rlw = rowL_of(f, d, w);
             int cl = 0;
+            BC_LOOP
             for (int x2 = 0; x2 < WL; x2++) cl += __popc(Ls[x2] & rlo[x2] & rlw[x2]);
             keep = cl >= need_g;
           }
@@ -904,6 +941,7 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
     ncand = ncand_eval = compact_bits(Ls, WL, f.cand);
   } else {  // batches count every candidate; only survivors are evaluated
     int c = 0;
+    BC_LOOP
     for (int w = lane; w < WL; w += 32) c += __popc(Ls[w]);
     ncand = __reduce_add_sync(FULL, c);
     ncand_eval = compact_bits_and(Ls, f.s1, WL, f.cand);
@@ -914,6 +952,7 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
   int ns = 0;
   const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
   int *out = f.surv + li * f.surv_cap;
+  BC_LOOP
   for (int c0 = 0; c0 < ncand_eval; c0 += 32) {
     const int i = c0 + lane;
     bool keep = false;
@@ -923,6 +962,7 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
       const uint32_t *row = rowR_of(f, d, u);
       int cr = 0;
       if (row)
+        BC_LOOP
         for (int w = 0; w < WR; w++) cr += __popc(R[w] & row[w]);
       if (INSTR) {
         tl.inter++;
@@ -943,6 +983,7 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
           } else {
             const uint32_t *rl = rowL_of(f, d, u);
             int cl = 0;
+            BC_LOOP
             for (int w = 0; w < WL; w++) cl += __popc(Ls[w] & rl[w]);
             keep = cl >= need_l;
           }
@@ -1010,7 +1051,9 @@ __device__ __forceinline__ bool emit_node(const Params &P, const SplitSink &S, c
     rec[2] = (uint32_t)(S.frame_off & 0xffffffffll);
     rec[3] = (uint32_t)(S.frame_off >> 32);
   }
+  BC_LOOP
   for (int w = lane; w < d.WR; w += 32) rec[4 + w] = R[w] & rr[w];
+  BC_LOOP
   for (int w = lane; w < d.WL; w += 32) rec[4 + d.WR + w] = Ls[w] & rl[w];
   __syncwarp();
   return true;
@@ -1029,6 +1072,7 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
   long long work = 0;
   int level = start;
   bool fresh = true;  // one expand call site: the kernel stays small (I-cache)
+  BC_LOOP
   for (;;) {
     if (fresh) {
       work += expand<INSTR, LAZY>(P, f, d, level, map, lb, acc, tl, ph_);
@@ -1054,7 +1098,9 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
       if (sink && level + 1 == sink->level &&
           emit_node(P, *sink, d, level + 1, f.setR + li * WR, rr, f.setL + li * WL, rl))
         continue;
+      BC_LOOP
       for (int w = lane; w < WR; w += 32) f.setR[(li + 1) * WR + w] = f.setR[li * WR + w] & rr[w];
+      BC_LOOP
       for (int w = lane; w < WL; w += 32) f.setL[(li + 1) * WL + w] = f.setL[li * WL + w] & rl[w];
       __syncwarp();
       level++;
@@ -1073,6 +1119,7 @@ __device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int 
                                            uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
   const int lane = lane_id();
   int pos = 0;
+  BC_LOOP
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
     uint32_t word = 0;
@@ -1084,6 +1131,7 @@ __device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int 
     const unsigned m = __ballot_sync(FULL, start);
     if (start) {
       uint32_t v = 0;
+      BC_LOOP
       for (int k = i; k < n; k++) {
         const uint32_t id = (uint32_t)__ldg(ids + k);
         if ((id >> 5) != word) break;
@@ -1117,6 +1165,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
                                                 int64_t lbase, F fn) {
   const int lane = lane_id();
   const int32_t *__restrict__ src = P.lseg ? P.rrows : P.g.bidx;
+  BC_LOOP
   for (int b0 = 0; b0 < d.nR; b0 += 32) {
     const int i = b0 + lane;
     int64_t start = 0;
@@ -1141,6 +1190,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
     const int excl = incl - len;
     const int T = __shfl_sync(FULL, incl, 31);
     constexpr int U = 4;  // gathers in flight per lane
+    BC_LOOP
     for (int r0 = 0; r0 < T; r0 += 32 * U) {
       int xs[U], own[U];
 #pragma unroll
@@ -1192,22 +1242,26 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
   isect_dir<true>(P.g, r, s, card, f.l_idx, f.l_val, f.l_pre);
   PH_MARK(1);
   // decode C_L1 ids (ascending, htb.py:42-52); fill the slot map
+  BC_LOOP
   for (int k = lane; k < d.wL; k += 32) {
     uint32_t v = f.l_val[k];
     const int base_id = (int)f.l_idx[k] * 32;
     int pos = f.l_pre[k];
     if (map) map[f.l_idx[k]] = (uint16_t)k;
     if (!sp.compact)
+      BC_LOOP
       while (v) {
         f.lids[pos++] = base_id + __ffs(v) - 1;
         v &= v - 1;
       }
   }
   if (sp.compact) {  // C_R1 members, ascending
+    BC_LOOP
     for (int k = lane; k < d.wR; k += 32) {
       uint32_t v = f.r_val[k];
       const int base_id = (int)f.r_idx[k] * 32;
       int pos = f.r_pre[k];
+      BC_LOOP
       while (v) {
         f.rids[pos++] = base_id + __ffs(v) - 1;
         v &= v - 1;
@@ -1218,12 +1272,14 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
   PH_MARK(2);
   int ns1 = 0;
   if (sp.compact) {
+    BC_LOOP
     for (int x = lane; x < d.nL; x += 32) f.lslot[x] = 0;
     __syncwarp();
     int *cnt = f.lslot;
     const int64_t lbase = P.lseg ? P.roff[j] : 0;
     for_member_hits(P, f, d, f.rids, map, lbase, [&](int, int lx) { atomicAdd(cnt + lx, 1); });
     int base = 0;
+    BC_LOOP
     for (int x0 = 0; x0 < d.nL; x0 += 32) {
       const int x = x0 + lane;
       const bool sv = x < d.nL && f.lslot[x] >= P.q_eff;
@@ -1235,6 +1291,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     __syncwarp();
     if (ROWS && ns1 > 0 && ns1 <= sp.rows(d.nL)) {
       const int64_t total = (int64_t)ns1 * d.WR;
+      BC_LOOP
       for (int64_t w = lane; w < total; w += 32) f.rowR[w] = 0;
       __syncwarp();
       uint32_t *rowR = f.rowR;
@@ -1246,6 +1303,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
       });
     }
   } else {
+    BC_LOOP
     for (int x = lane; x < d.nL; x += 32) {
       const int id = f.lids[x];
       const int sl = P.g.dense_id[id];
@@ -1256,12 +1314,14 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     __syncwarp();
     if (!sp.lslot()) return -1;  // survivors not needed (no rowL rows, no triage)
     int base = 0;
+    BC_LOOP
     for (int x0 = 0; x0 < d.nL; x0 += 32) {
       const int x = x0 + lane;
       bool sv = false;
       if (x < d.nL) {
         const uint32_t *row = f.rowR + (int64_t)x * d.WR;
         int c = 0;
+        BC_LOOP
         for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
         sv = c >= P.q_eff;
       }
@@ -1285,15 +1345,19 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
   // word-boundary masks of the local universes for the batch accounting below level 1
   // (C_R: leaf-parents and deeper nodes; C_L: nodes at level >= 2, p_eff >= 5)
   const bool need_l = P.p_eff >= 5;
+  BC_LOOP
   for (int w = lane; w < d.WR; w += 32) f.r_last[w] = 0;
   if (need_l)
+    BC_LOOP
     for (int w = lane; w < d.WL; w += 32) f.l_last[w] = 0;
   __syncwarp();
+  BC_LOOP
   for (int k = lane; k < d.wR; k += 32) {
     const int e = f.r_pre[k + 1] - 1;
     atomicOr(f.r_last + (e >> 5), 1u << (e & 31));
   }
   if (need_l)
+    BC_LOOP
     for (int k = lane; k < d.wL; k += 32) {
       const int e = f.l_pre[k + 1] - 1;
       atomicOr(f.l_last + (e >> 5), 1u << (e & 31));
@@ -1302,6 +1366,7 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
   // level-1 R-survivor masks: candidates outside them cannot pass |R & N(x)| >= q.
   // Used in compact mode (few survivors among many candidates, e.g. hub pairs);
   // where most candidates survive the extra masks do not pay.
+  BC_LOOP
   for (int x0 = 0; sp.compact && x0 < d.nL; x0 += 32) {
     const int x = x0 + lane;
     bool sv = false;
@@ -1311,6 +1376,7 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
       } else {
         const uint32_t *row = f.rowR + (int64_t)x * d.WR;
         int c = 0;
+        BC_LOOP
         for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
         sv = c >= P.q_eff;
       }
@@ -1319,9 +1385,11 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
     if (lane == 0) f.s1[x0 >> 5] = m;
   }
   __syncwarp();
+  BC_LOOP
   for (int k = lane; sp.compact && k < d.wL; k += 32) {
     uint32_t v = f.l_val[k], h = 0;
     int pos = f.l_pre[k];
+    BC_LOOP
     while (v) {
       const int b = __ffs(v) - 1;
       v &= v - 1;
@@ -1336,6 +1404,7 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
     PH_MARK(3);
     return;
   }
+  BC_LOOP
   for (int x = lane; x < d.nL; x += 32) {
     if (sp.compact && !INSTR && f.lslot[x] < 0) continue;
     const int id = lid_of(f, d, x);
@@ -1362,16 +1431,19 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
 
 __device__ __forceinline__ void clear_map(uint16_t *map, const Frame &f, const Dims &d) {
   if (!map) return;
+  BC_LOOP
   for (int k = lane_id(); k < d.wL; k += 32) map[f.l_idx[k]] = 0xffff;
   __syncwarp();
 }
 
 __device__ __forceinline__ void init_root_sets(const Frame &f, const Dims &d) {
   const int lane = lane_id();
+  BC_LOOP
   for (int w = lane; w < d.WR; w += 32) {
     const int rem = d.nR - w * 32;
     f.setR[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
   }
+  BC_LOOP
   for (int w = lane; w < d.WL; w += 32) {
     const int rem = d.nL - w * 32;
     f.setL[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
@@ -1465,6 +1537,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
   uint32_t *my_smem = my + map_w + LEAF_WORDS;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   if (map)
+    BC_LOOP
     for (int i = lane; i < map_w; i += 32) my[i] = 0xffffffffu;
   __syncwarp();
   Acc128 total{0, 0};
@@ -1472,6 +1545,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
   unsigned long long claims = 0, spills = 0;
   const int p_eff = P.p_eff;
   PH_DECL
+  BC_LOOP
   for (;;) {
     long long qi = 0;
     if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
@@ -1575,6 +1649,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
   unsigned long long spills = 0;
   const int p_eff = P.p_eff;
   PH_DECL
+  BC_LOOP
   for (;;) {
     long long k = 0;
     if (lane == 0) k = (long long)atomicAdd(P.ctr + CTR_SUB_NEXT, 1ull);
@@ -1597,7 +1672,9 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
     Frame f;
     carve_ro(f, A.frames + foff, d, sp);
     carve_scratch(f, sc_base, d, p_eff, sp);
+    BC_LOOP
     for (int w = lane; w < d.WR; w += 32) f.setR[(lv - 1) * d.WR + w] = rec[4 + w];
+    BC_LOOP
     for (int w = lane; w < d.WL; w += 32) f.setL[(lv - 1) * d.WL + w] = rec[4 + d.WR + w];
     __syncwarp();
     Acc128 acc{0, 0};
@@ -1631,6 +1708,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, FILTER_MIN_BLOCKS) filter_kernel
   uint32_t *my_smem = my + map_w;
   uint32_t *my_global = A.gscratch ? A.gscratch + gwarp * A.gscratch_words : nullptr;
   if (map)
+    BC_LOOP
     for (int i = lane; i < map_w; i += 32) my[i] = 0xffffffffu;
   __syncwarp();
   Tally tl;
@@ -1638,6 +1716,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, FILTER_MIN_BLOCKS) filter_kernel
   unsigned long long claims = 0;
   const int p_eff = P.p_eff;
   PH_DECL
+  BC_LOOP
   for (;;) {
     long long qi = 0;
     if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
