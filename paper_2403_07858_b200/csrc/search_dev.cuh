@@ -603,6 +603,13 @@ struct Tally {
   unsigned long long batches = 0, inter = 0, opw = 0, minw = 0;
 };
 
+// several batches: the divisions stay out of line (one copy, off the hot path)
+static __device__ __noinline__ unsigned node_batches_div(unsigned ncand, unsigned wm, unsigned cap) {
+  unsigned b = cap / wm;
+  if (b < 1) b = 1;
+  return (ncand + b - 1) / b;
+}
+
 // reference batch count for one node expansion (engine.py:306-313, 329-331)
 __device__ __forceinline__ unsigned node_batches(const Params &P, unsigned ncand, int wr, int wl,
                                                  bool leaf) {
@@ -612,9 +619,7 @@ __device__ __forceinline__ unsigned node_batches(const Params &P, unsigned ncand
   const unsigned w = (unsigned)(wr > 1 ? wr : 1), w2 = leaf ? 1u : (unsigned)(wl > 1 ? wl : 1);
   const unsigned wm = w > w2 ? w : w2;  // b = cap / max(wr, wl)
   if ((unsigned long long)ncand * wm <= cap) return 1;  // one batch: no division
-  unsigned b = cap / wm;
-  if (b < 1) b = 1;
-  return (ncand + b - 1) / b;
+  return node_batches_div(ncand, wm, cap);
 }
 
 // Per-warp shared-memory staging of (leaf-parent slot, leaf) pairs.
