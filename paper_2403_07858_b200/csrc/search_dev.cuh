@@ -259,23 +259,37 @@ struct FrameSpec {
 };
 
 struct Frame {
-  uint32_t *r_idx, *r_val;
-  int *r_pre;
-  uint32_t *l_idx, *l_val;
-  int *l_pre;
-  uint32_t *r_last;  // bit i: local C_R1 index i is the last of its HTB word
-  uint32_t *l_last;  // same for C_L1
-  uint32_t *s1;      // level-1 R-survivors as a bitset over the local C_L1 indices
-  uint32_t *s1h;     // the same per C_L1 HTB word (bits of l_val that are survivors)
-  int *lids, *lslot, *rids;
-  uint32_t *rowR, *rowL;
-  int *adjw, *dirw;
-  int *cand;
-  uint32_t *setR, *setL;
-  int *surv;
-  int *ns, *cur;
+  // two bases and 32-bit word offsets (frames are far below 2^31 words): row and set
+  // addresses are one 32-bit multiply-add and one wide add, not 64-bit pointer math
+  uint32_t *ro;  // read-only part (built once; split tasks share it from the arena)
+  uint32_t *sc;  // per-warp DFS scratch
+  int o_r_idx, o_r_val, o_r_pre, o_l_idx, o_l_val, o_l_pre, o_r_last, o_l_last, o_s1, o_s1h, o_lids, o_lslot, o_rids, o_rowR, o_rowL, o_adjw, o_dirw;
+  int o_cand, o_setR, o_setL, o_surv, o_ns, o_cur;
   int surv_cap;
   bool compact;
+  __device__ __forceinline__ uint32_t *r_idx() const { return (uint32_t *)(ro + o_r_idx); }
+  __device__ __forceinline__ uint32_t *r_val() const { return (uint32_t *)(ro + o_r_val); }
+  __device__ __forceinline__ int *r_pre() const { return (int *)(ro + o_r_pre); }
+  __device__ __forceinline__ uint32_t *l_idx() const { return (uint32_t *)(ro + o_l_idx); }
+  __device__ __forceinline__ uint32_t *l_val() const { return (uint32_t *)(ro + o_l_val); }
+  __device__ __forceinline__ int *l_pre() const { return (int *)(ro + o_l_pre); }
+  __device__ __forceinline__ uint32_t *r_last() const { return (uint32_t *)(ro + o_r_last); }
+  __device__ __forceinline__ uint32_t *l_last() const { return (uint32_t *)(ro + o_l_last); }
+  __device__ __forceinline__ uint32_t *s1() const { return (uint32_t *)(ro + o_s1); }
+  __device__ __forceinline__ uint32_t *s1h() const { return (uint32_t *)(ro + o_s1h); }
+  __device__ __forceinline__ int *lids() const { return (int *)(ro + o_lids); }
+  __device__ __forceinline__ int *lslot() const { return (int *)(ro + o_lslot); }
+  __device__ __forceinline__ int *rids() const { return (int *)(ro + o_rids); }
+  __device__ __forceinline__ uint32_t *rowR() const { return (uint32_t *)(ro + o_rowR); }
+  __device__ __forceinline__ uint32_t *rowL() const { return (uint32_t *)(ro + o_rowL); }
+  __device__ __forceinline__ int *adjw() const { return (int *)(ro + o_adjw); }
+  __device__ __forceinline__ int *dirw() const { return (int *)(ro + o_dirw); }
+  __device__ __forceinline__ int *cand() const { return (int *)(sc + o_cand); }
+  __device__ __forceinline__ uint32_t *setR() const { return (uint32_t *)(sc + o_setR); }
+  __device__ __forceinline__ uint32_t *setL() const { return (uint32_t *)(sc + o_setL); }
+  __device__ __forceinline__ int *surv() const { return (int *)(sc + o_surv); }
+  __device__ __forceinline__ int *ns() const { return (int *)(sc + o_ns); }
+  __device__ __forceinline__ int *cur() const { return (int *)(sc + o_cur); }
 };
 
 // rowL is materialised for p_eff >= 5 (reused at every depth) and for p_eff = 4
@@ -325,23 +339,25 @@ __host__ __device__ __forceinline__ int64_t scratch_words(int nR, int nL, int p_
 
 __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d,
                                          const FrameSpec &sp) {
-  f.r_idx = p; p += d.wR;
-  f.r_val = p; p += d.wR;
-  f.r_pre = (int *)p; p += d.wR + 1;
-  f.l_idx = p; p += d.wL;
-  f.l_val = p; p += d.wL;
-  f.l_pre = (int *)p; p += d.wL + 1;
-  f.r_last = p; p += d.WR;
-  f.l_last = p; p += d.WL;
-  f.s1 = p; if (sp.compact) p += d.WL;
-  f.s1h = p; if (sp.compact) p += d.wL;
-  f.lids = (int *)p; if (!sp.compact) p += d.nL;
-  f.lslot = (int *)p; if (sp.lslot()) p += d.nL;
-  f.rids = (int *)p; if (sp.compact) p += d.nR;
-  f.rowR = p; p += (sp.compact ? sp.rows(d.nL) : d.nL) * d.WR;
-  f.rowL = p; if (sp.rowL) p += sp.rows(d.nL) * d.WL;
-  f.adjw = (int *)p; if (sp.instr) p += d.nL;
-  f.dirw = (int *)p;
+  int o = 0;
+  f.ro = p;
+  f.o_r_idx = o; o += d.wR;
+  f.o_r_val = o; o += d.wR;
+  f.o_r_pre = o; o += d.wR + 1;
+  f.o_l_idx = o; o += d.wL;
+  f.o_l_val = o; o += d.wL;
+  f.o_l_pre = o; o += d.wL + 1;
+  f.o_r_last = o; o += d.WR;
+  f.o_l_last = o; o += d.WL;
+  f.o_s1 = o; if (sp.compact) o += d.WL;
+  f.o_s1h = o; if (sp.compact) o += d.wL;
+  f.o_lids = o; if (!sp.compact) o += d.nL;
+  f.o_lslot = o; if (sp.lslot()) o += d.nL;
+  f.o_rids = o; if (sp.compact) o += d.nR;
+  f.o_rowR = o; o += (int)(sp.compact ? sp.rows(d.nL) : d.nL) * d.WR;
+  f.o_rowL = o; if (sp.rowL) o += (int)sp.rows(d.nL) * d.WL;
+  f.o_adjw = o; if (sp.instr) o += d.nL;
+  f.o_dirw = o;
   f.compact = sp.compact;
 }
 
@@ -349,37 +365,39 @@ __device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims 
                                               const FrameSpec &sp) {
   const int levels = stack_levels(p_eff);
   f.surv_cap = (int)sp.rows(d.nL);
-  f.cand = (int *)p; p += d.nL;
-  f.setR = p; p += (int64_t)levels * d.WR;
-  f.setL = p; p += (int64_t)levels * d.WL;
-  f.surv = (int *)p; p += (int64_t)levels * f.surv_cap;
-  f.ns = (int *)p; p += levels;
-  f.cur = (int *)p;
+  int o = 0;
+  f.sc = p;
+  f.o_cand = o; o += d.nL;
+  f.o_setR = o; o += levels * d.WR;
+  f.o_setL = o; o += levels * d.WL;
+  f.o_surv = o; o += levels * f.surv_cap;
+  f.o_ns = o; o += levels;
+  f.o_cur = o;
 }
 
 __device__ __forceinline__ const uint32_t *rowL_of(const Frame &f, const Dims &d, int u) {
-  return f.rowL + (int64_t)f.lslot[u] * d.WL;
+  return f.ro + (f.o_rowL + f.lslot()[u] * d.WL);
 }
 
 // anchor id of C_L1 local index x: decoded list (full mode) or, in compact mode,
 // the word holding x (bisect on the prefix counts) and its bit of that rank
 __device__ __forceinline__ int lid_of(const Frame &f, const Dims &d, int x) {
-  if (!f.compact) return f.lids[x];
+  if (!f.compact) return f.lids()[x];
   int lo = 0, hi = d.wL - 1;
   BC_LOOP
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (f.l_pre[mid] <= x) lo = mid;
+    if (f.l_pre()[mid] <= x) lo = mid;
     else hi = mid - 1;
   }
-  return (int)f.l_idx[lo] * 32 + (int)__fns(f.l_val[lo], 0, x - f.l_pre[lo] + 1);
+  return (int)f.l_idx()[lo] * 32 + (int)__fns(f.l_val()[lo], 0, x - f.l_pre()[lo] + 1);
 }
 
 // rowR of candidate u, or null when u has no row (not a level-1 R-survivor)
 __device__ __forceinline__ const uint32_t *rowR_of(const Frame &f, const Dims &d, int u) {
-  if (!f.compact) return f.rowR + (int64_t)u * d.WR;
-  const int sl = f.lslot[u];
-  return sl >= 0 ? f.rowR + (int64_t)sl * d.WR : nullptr;
+  if (!f.compact) return f.ro + (f.o_rowR + u * d.WR);
+  const int sl = f.lslot()[u];
+  return sl >= 0 ? f.ro + (f.o_rowR + sl * d.WR) : nullptr;
 }
 
 // Writes a local-universe row whose set positions arrive in ascending order:
@@ -690,8 +708,8 @@ __device__ __forceinline__ void eval_leaves(const Params &P, const Frame &f, con
       }
       if (INSTR) {
         tl.inter++;
-        tl.opw += wro + f.adjw[w];
-        tl.minw += wro < f.adjw[w] ? wro : f.adjw[w];
+        tl.opw += wro + f.adjw()[w];
+        tl.minw += wro < f.adjw()[w] ? wro : f.adjw()[w];
       }
       if (c >= P.q_eff) add_comb(P, acc, c);
     }
@@ -712,8 +730,8 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
                                              Tally &tl, const int *list2 = nullptr) {
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL;
-  const uint32_t *R = f.setR + (level - 1) * WR;
-  const uint32_t *Ls = f.setL + (level - 1) * WL;
+  const uint32_t *R = f.setR() + (level - 1) * WR;
+  const uint32_t *Ls = f.setL() + (level - 1) * WL;
   BC_LOOP
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
@@ -721,7 +739,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     const int u = act ? list[i] : 0;
     const uint32_t *ru_mine = act ? rowR_of(f, d, u) : nullptr;
     const uint32_t *ru2 = act && list2 ? rowR_of(f, d, list2[i]) : nullptr;
-    const int wr = act ? lane_words(R, ru_mine, f.r_last, WR, ru2) : 0;
+    const int wr = act ? lane_words(R, ru_mine, f.r_last(), WR, ru2) : 0;
     uint32_t rp[RP_WORDS];
 #pragma unroll
     for (int x = 0; x < RP_WORDS; x++)
@@ -765,25 +783,25 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
           const uint32_t key = __ldg(P.g.didx + j), dv = __ldg(P.g.dval + j);
           const int k = map[key];
           if (k != 0xffff) {
-            v = f.l_val[k];
+            v = f.l_val()[k];
             m = v & dv;
-            pre = f.l_pre[k];
+            pre = f.l_pre()[k];
             if (m) atomicAdd(&lb.ncand[sl], __popc(m));
-            if (!INSTR && f.compact) m &= f.s1h[k];  // non-survivor leaves add 0
+            if (!INSTR && f.compact) m &= f.s1h()[k];  // non-survivor leaves add 0
           }
         }
         eval_leaves<INSTR>(P, f, d, R, list + base, sl, v, pre, m, lb.wr[sl], rp, acc, tl);
       }
     } else {
       int ncand = 0;
-      const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL;
+      const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL();
       const uint32_t *rl2 = act && list2 ? rowL_of(f, d, list2[i]) : nullptr;
       BC_LOOP
       for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
         uint32_t m = 0;
         if (act && x < WL) m = Ls[x] & rl[x] & (rl2 ? rl2[x] : FULL);
         ncand += __popc(m);
-        if (!INSTR && f.compact) m &= f.s1[x];
+        if (!INSTR && f.compact) m &= f.s1()[x];
         eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, rp, acc,
                            tl);
       }
@@ -809,10 +827,10 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL;
   const int li = level - 1;
-  const uint32_t *R = f.setR + li * WR;
-  const uint32_t *Ls = f.setL + li * WL;
-  const int n = f.ns[li];
-  const int *kids = f.surv + li * f.surv_cap;
+  const uint32_t *R = f.setR() + li * WR;
+  const uint32_t *Ls = f.setL() + li * WL;
+  const int n = f.ns()[li];
+  const int *kids = f.surv() + li * f.surv_cap;
   const int need_g = P.p_eff - level - 3;  // prune_keep at level + 2
   int work = 0, fill = 0;
   BC_LOOP
@@ -821,18 +839,18 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
     const bool act = i < n;
     const int u = act ? kids[i] : 0;
     const uint32_t *ru = act ? rowR_of(f, d, u) : nullptr;
-    const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL;
+    const uint32_t *rl = act ? rowL_of(f, d, u) : f.rowL();
     uint32_t rp[RP_WORDS];
 #pragma unroll
     for (int x = 0; x < RP_WORDS; x++) rp[x] = act && x < WR ? R[x] & ru[x] : 0u;
-    const int wr_u = act ? lane_words(R, ru, f.r_last, WR) : 0;
-    const int wl_u = act ? lane_words(Ls, rl, f.l_last, WL) : 0;
+    const int wr_u = act ? lane_words(R, ru, f.r_last(), WR) : 0;
+    const int wl_u = act ? lane_words(Ls, rl, f.l_last(), WL) : 0;
     int ncand_u = 0;
     BC_LOOP
     for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
       const uint32_t mall = act && x < WL ? Ls[x] & rl[x] : 0u;
       ncand_u += __popc(mall);
-      const uint32_t m = INSTR || !f.compact ? mall : mall & f.s1[x];
+      const uint32_t m = INSTR || !f.compact ? mall : mall & f.s1()[x];
       const int cnt = __popc(m);
       int incl = cnt;
 #pragma unroll
@@ -873,14 +891,14 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
           }
           if (INSTR) {
             tl.inter++;
-            tl.opw += wro + f.adjw[w];
-            tl.minw += wro < f.adjw[w] ? wro : f.adjw[w];
+            tl.opw += wro + f.adjw()[w];
+            tl.minw += wro < f.adjw()[w] ? wro : f.adjw()[w];
           }
           if (cr >= P.q_eff) {
             if (INSTR) {
               tl.inter++;
-              tl.opw += wlo + f.dirw[w];
-              tl.minw += wlo < f.dirw[w] ? wlo : f.dirw[w];
+              tl.opw += wlo + f.dirw()[w];
+              tl.minw += wlo < f.dirw()[w] ? wlo : f.dirw()[w];
             }
             const uint32_t *rlo = rowL_of(f, d, uo), *rlw = rowL_of(f, d, w);
             int cl = 0;
@@ -937,33 +955,33 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
   const int lane = lane_id();
   const int WR = d.WR, WL = d.WL, nL = d.nL;
   const int li = level - 1;
-  const uint32_t *R = f.setR + li * WR;
-  const uint32_t *Ls = f.setL + li * WL;
+  const uint32_t *R = f.setR() + li * WR;
+  const uint32_t *Ls = f.setL() + li * WL;
   const bool leaf = level + 1 == P.p_eff - 1;
   const bool lp = level + 1 == P.p_eff - 2;  // children are leaf-parents
   int ncand, ncand_eval;
   if (INSTR || !f.compact) {
-    ncand = ncand_eval = compact_bits(Ls, WL, f.cand);
+    ncand = ncand_eval = compact_bits(Ls, WL, f.cand());
   } else {  // batches count every candidate; only survivors are evaluated
     int c = 0;
     BC_LOOP
     for (int w = lane; w < WL; w += 32) c += __popc(Ls[w]);
     ncand = __reduce_add_sync(FULL, c);
-    ncand_eval = compact_bits_and(Ls, f.s1, WL, f.cand);
+    ncand_eval = compact_bits_and(Ls, f.s1(), WL, f.cand());
   }
-  const int wr = level == 1 ? d.wR : words_touched(R, f.r_last, WR);
-  const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_last, WL));
+  const int wr = level == 1 ? d.wR : words_touched(R, f.r_last(), WR);
+  const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_last(), WL));
   if (lane == 0) tl.batches += node_batches(P, (unsigned)ncand, wr, wl, leaf);
   int ns = 0;
   const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
-  int *out = f.surv + li * f.surv_cap;
+  int *out = f.surv() + li * f.surv_cap;
   BC_LOOP
   for (int c0 = 0; c0 < ncand_eval; c0 += 32) {
     const int i = c0 + lane;
     bool keep = false;
     int u = 0;
     if (i < ncand_eval) {
-      u = f.cand[i];
+      u = f.cand()[i];
       const uint32_t *row = rowR_of(f, d, u);
       int cr = 0;
       if (row)
@@ -971,8 +989,8 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
         for (int w = 0; w < WR; w++) cr += __popc(R[w] & row[w]);
       if (INSTR) {
         tl.inter++;
-        tl.opw += wr + f.adjw[u];
-        tl.minw += wr < f.adjw[u] ? wr : f.adjw[u];
+        tl.opw += wr + f.adjw()[u];
+        tl.minw += wr < f.adjw()[u] ? wr : f.adjw()[u];
       }
       if (cr >= P.q_eff) {
         if (leaf) {
@@ -980,8 +998,8 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
         } else {
           if (INSTR) {
             tl.inter++;
-            tl.opw += wl + f.dirw[u];
-            tl.minw += wl < f.dirw[u] ? wl : f.dirw[u];
+            tl.opw += wl + f.dirw()[u];
+            tl.minw += wl < f.dirw()[u] ? wl : f.dirw()[u];
           }
           if (LAZY) {
             keep = true;  // |L'| >= 1 is checked when the leaf-parent is walked
@@ -1011,8 +1029,8 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
     ns = 0;
   }
   if (lane == 0) {
-    f.ns[li] = ns;
-    f.cur[li] = 0;
+    f.ns()[li] = ns;
+    f.cur()[li] = 0;
   }
   __syncwarp();
   return work;
@@ -1084,29 +1102,29 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
       if (work > limit) return false;
       fresh = false;
       const int li0 = level - 1;
-      if (FLAT && !LAZY && level + 2 == p_eff - 2 && WR <= RP_WORDS && f.ns[li0] > 0 &&
+      if (FLAT && !LAZY && level + 2 == p_eff - 2 && WR <= RP_WORDS && f.ns()[li0] > 0 &&
           !(sink && level + 1 == sink->level)) {
         // the children's children are leaf-parents: expand every child at once
         work += expand_children<INSTR>(P, f, d, level, lb, acc, tl);
         if (work > limit) return false;
-        if (lane == 0) f.ns[li0] = 0;
+        if (lane == 0) f.ns()[li0] = 0;
         __syncwarp();
       }
     }
     const int li = level - 1;
-    if (level + 1 < p_eff - 2 && f.cur[li] < f.ns[li]) {
-      const int u = f.surv[li * f.surv_cap + f.cur[li]];
+    if (level + 1 < p_eff - 2 && f.cur()[li] < f.ns()[li]) {
+      const int u = f.surv()[li * f.surv_cap + f.cur()[li]];
       __syncwarp();
-      if (lane == 0) f.cur[li]++;
+      if (lane == 0) f.cur()[li]++;
       const uint32_t *rr = rowR_of(f, d, u);
       const uint32_t *rl = rowL_of(f, d, u);
       if (sink && level + 1 == sink->level &&
-          emit_node(P, *sink, d, level + 1, f.setR + li * WR, rr, f.setL + li * WL, rl))
+          emit_node(P, *sink, d, level + 1, f.setR() + li * WR, rr, f.setL() + li * WL, rl))
         continue;
       BC_LOOP
-      for (int w = lane; w < WR; w += 32) f.setR[(li + 1) * WR + w] = f.setR[li * WR + w] & rr[w];
+      for (int w = lane; w < WR; w += 32) f.setR()[(li + 1) * WR + w] = f.setR()[li * WR + w] & rr[w];
       BC_LOOP
-      for (int w = lane; w < WL; w += 32) f.setL[(li + 1) * WL + w] = f.setL[li * WL + w] & rl[w];
+      for (int w = lane; w < WL; w += 32) f.setL()[(li + 1) * WL + w] = f.setL()[li * WL + w] & rl[w];
       __syncwarp();
       level++;
       fresh = true;
@@ -1219,9 +1237,9 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
         if (x < 0) continue;
         const int k = map[x >> 5];
         if (k != 0xffff) {
-          const uint32_t lv = f.l_val[k];
+          const uint32_t lv = f.l_val()[k];
           const int xb = x & 31;
-          if ((lv >> xb) & 1u) fn(b0 + own[u], f.l_pre[k] + __popc(lv & ((1u << xb) - 1u)));
+          if ((lv >> xb) & 1u) fn(b0 + own[u], f.l_pre()[k] + __popc(lv & ((1u << xb) - 1u)));
         }
       }
     }
@@ -1242,33 +1260,33 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
                                              uint16_t *map, PhaseClock &ph_) {
   const int lane = lane_id();
   int card;
-  if (P.lists) list_to_htb(P.lists + P.roff[j], d.nR, f.r_idx, f.r_val, f.r_pre);
-  else isect_adj<true>(P.g, r, s, card, f.r_idx, f.r_val, f.r_pre);
-  isect_dir<true>(P.g, r, s, card, f.l_idx, f.l_val, f.l_pre);
+  if (P.lists) list_to_htb(P.lists + P.roff[j], d.nR, f.r_idx(), f.r_val(), f.r_pre());
+  else isect_adj<true>(P.g, r, s, card, f.r_idx(), f.r_val(), f.r_pre());
+  isect_dir<true>(P.g, r, s, card, f.l_idx(), f.l_val(), f.l_pre());
   PH_MARK(1);
   // decode C_L1 ids (ascending, htb.py:42-52); fill the slot map
   BC_LOOP
   for (int k = lane; k < d.wL; k += 32) {
-    uint32_t v = f.l_val[k];
-    const int base_id = (int)f.l_idx[k] * 32;
-    int pos = f.l_pre[k];
-    if (map) map[f.l_idx[k]] = (uint16_t)k;
+    uint32_t v = f.l_val()[k];
+    const int base_id = (int)f.l_idx()[k] * 32;
+    int pos = f.l_pre()[k];
+    if (map) map[f.l_idx()[k]] = (uint16_t)k;
     if (!sp.compact)
       BC_LOOP
       while (v) {
-        f.lids[pos++] = base_id + __ffs(v) - 1;
+        f.lids()[pos++] = base_id + __ffs(v) - 1;
         v &= v - 1;
       }
   }
   if (sp.compact) {  // C_R1 members, ascending
     BC_LOOP
     for (int k = lane; k < d.wR; k += 32) {
-      uint32_t v = f.r_val[k];
-      const int base_id = (int)f.r_idx[k] * 32;
-      int pos = f.r_pre[k];
+      uint32_t v = f.r_val()[k];
+      const int base_id = (int)f.r_idx()[k] * 32;
+      int pos = f.r_pre()[k];
       BC_LOOP
       while (v) {
-        f.rids[pos++] = base_id + __ffs(v) - 1;
+        f.rids()[pos++] = base_id + __ffs(v) - 1;
         v &= v - 1;
       }
     }
@@ -1278,18 +1296,18 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
   int ns1 = 0;
   if (sp.compact) {
     BC_LOOP
-    for (int x = lane; x < d.nL; x += 32) f.lslot[x] = 0;
+    for (int x = lane; x < d.nL; x += 32) f.lslot()[x] = 0;
     __syncwarp();
-    int *cnt = f.lslot;
+    int *cnt = f.lslot();
     const int64_t lbase = P.lseg ? P.roff[j] : 0;
-    for_member_hits(P, f, d, f.rids, map, lbase, [&](int, int lx) { atomicAdd(cnt + lx, 1); });
+    for_member_hits(P, f, d, f.rids(), map, lbase, [&](int, int lx) { atomicAdd(cnt + lx, 1); });
     int base = 0;
     BC_LOOP
     for (int x0 = 0; x0 < d.nL; x0 += 32) {
       const int x = x0 + lane;
-      const bool sv = x < d.nL && f.lslot[x] >= P.q_eff;
+      const bool sv = x < d.nL && f.lslot()[x] >= P.q_eff;
       const unsigned m = __ballot_sync(FULL, sv);
-      if (x < d.nL) f.lslot[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
+      if (x < d.nL) f.lslot()[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
       base += __popc(m);
     }
     ns1 = base;
@@ -1297,24 +1315,24 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     if (ROWS && ns1 > 0 && ns1 <= sp.rows(d.nL)) {
       const int64_t total = (int64_t)ns1 * d.WR;
       BC_LOOP
-      for (int64_t w = lane; w < total; w += 32) f.rowR[w] = 0;
+      for (int64_t w = lane; w < total; w += 32) f.rowR()[w] = 0;
       __syncwarp();
-      uint32_t *rowR = f.rowR;
-      const int *lslot = f.lslot;
+      uint32_t *rowR = f.rowR();
+      const int *lslot = f.lslot();
       const int WR = d.WR;
-      for_member_hits(P, f, d, f.rids, map, lbase, [&](int i, int lx) {
+      for_member_hits(P, f, d, f.rids(), map, lbase, [&](int i, int lx) {
         const int sl = lslot[lx];
-        if (sl >= 0) atomicOr(rowR + (int64_t)sl * WR + (i >> 5), 1u << (i & 31));
+        if (sl >= 0) atomicOr(rowR + (sl * WR + (i >> 5)), 1u << (i & 31));
       });
     }
   } else {
     BC_LOOP
     for (int x = lane; x < d.nL; x += 32) {
-      const int id = f.lids[x];
+      const int id = f.lids()[x];
       const int sl = P.g.dense_id[id];
-      local_row(f.r_idx, f.r_val, f.r_pre, d.wR, P.g.aidx, P.g.aval, P.g.aoff[id],
+      local_row(f.r_idx(), f.r_val(), f.r_pre(), d.wR, P.g.aidx, P.g.aval, P.g.aoff[id],
                 P.g.aoff[id + 1], sl >= 0 ? P.g.dense + (int64_t)sl * P.g.mw : nullptr,
-                f.rowR + (int64_t)x * d.WR, d.WR);
+                f.rowR() + x * d.WR, d.WR);
     }
     __syncwarp();
     if (!sp.lslot()) return -1;  // survivors not needed (no rowL rows, no triage)
@@ -1324,14 +1342,14 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
       const int x = x0 + lane;
       bool sv = false;
       if (x < d.nL) {
-        const uint32_t *row = f.rowR + (int64_t)x * d.WR;
+        const uint32_t *row = f.rowR() + x * d.WR;
         int c = 0;
         BC_LOOP
         for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
         sv = c >= P.q_eff;
       }
       const unsigned m = __ballot_sync(FULL, sv);
-      if (x < d.nL) f.lslot[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
+      if (x < d.nL) f.lslot()[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
       base += __popc(m);
     }
     ns1 = base;
@@ -1351,21 +1369,21 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
   // (C_R: leaf-parents and deeper nodes; C_L: nodes at level >= 2, p_eff >= 5)
   const bool need_l = P.p_eff >= 5;
   BC_LOOP
-  for (int w = lane; w < d.WR; w += 32) f.r_last[w] = 0;
+  for (int w = lane; w < d.WR; w += 32) f.r_last()[w] = 0;
   if (need_l)
     BC_LOOP
-    for (int w = lane; w < d.WL; w += 32) f.l_last[w] = 0;
+    for (int w = lane; w < d.WL; w += 32) f.l_last()[w] = 0;
   __syncwarp();
   BC_LOOP
   for (int k = lane; k < d.wR; k += 32) {
-    const int e = f.r_pre[k + 1] - 1;
-    atomicOr(f.r_last + (e >> 5), 1u << (e & 31));
+    const int e = f.r_pre()[k + 1] - 1;
+    atomicOr(f.r_last() + (e >> 5), 1u << (e & 31));
   }
   if (need_l)
     BC_LOOP
     for (int k = lane; k < d.wL; k += 32) {
-      const int e = f.l_pre[k + 1] - 1;
-      atomicOr(f.l_last + (e >> 5), 1u << (e & 31));
+      const int e = f.l_pre()[k + 1] - 1;
+      atomicOr(f.l_last() + (e >> 5), 1u << (e & 31));
     }
   __syncwarp();
   // level-1 R-survivor masks: candidates outside them cannot pass |R & N(x)| >= q.
@@ -1377,9 +1395,9 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
     bool sv = false;
     if (x < d.nL) {
       if (sp.compact || sp.lslot()) {
-        sv = f.lslot[x] >= 0;
+        sv = f.lslot()[x] >= 0;
       } else {
-        const uint32_t *row = f.rowR + (int64_t)x * d.WR;
+        const uint32_t *row = f.rowR() + x * d.WR;
         int c = 0;
         BC_LOOP
         for (int w = 0; w < d.WR; w++) c += __popc(row[w]);
@@ -1387,21 +1405,21 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
       }
     }
     const unsigned m = __ballot_sync(FULL, sv);
-    if (lane == 0) f.s1[x0 >> 5] = m;
+    if (lane == 0) f.s1()[x0 >> 5] = m;
   }
   __syncwarp();
   BC_LOOP
   for (int k = lane; sp.compact && k < d.wL; k += 32) {
-    uint32_t v = f.l_val[k], h = 0;
-    int pos = f.l_pre[k];
+    uint32_t v = f.l_val()[k], h = 0;
+    int pos = f.l_pre()[k];
     BC_LOOP
     while (v) {
       const int b = __ffs(v) - 1;
       v &= v - 1;
-      if ((f.s1[pos >> 5] >> (pos & 31)) & 1u) h |= 1u << b;
+      if ((f.s1()[pos >> 5] >> (pos & 31)) & 1u) h |= 1u << b;
       pos++;
     }
-    f.s1h[k] = h;
+    f.s1h()[k] = h;
   }
   __syncwarp();
   const bool build = sp.rowL && P.p_eff >= 4 && !LAZY;
@@ -1411,23 +1429,23 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
   }
   BC_LOOP
   for (int x = lane; x < d.nL; x += 32) {
-    if (sp.compact && !INSTR && f.lslot[x] < 0) continue;
+    if (sp.compact && !INSTR && f.lslot()[x] < 0) continue;
     const int id = lid_of(f, d, x);
     if (build) {
-      const int slot = f.lslot[x];
+      const int slot = f.lslot()[x];
       if (slot >= 0) {
         const int64_t d0 = P.g.doff[id], d1 = P.g.doff[id + 1];
-        uint32_t *out = f.rowL + (int64_t)slot * d.WL;
+        uint32_t *out = f.rowL() + slot * d.WL;
         if (map)
-          local_row_map(map, f.l_val, f.l_pre, P.g.didx, P.g.dval, d0, d1, out, d.WL);
+          local_row_map(map, f.l_val(), f.l_pre(), P.g.didx, P.g.dval, d0, d1, out, d.WL);
         else
-          local_row(f.l_idx, f.l_val, f.l_pre, d.wL, P.g.didx, P.g.dval, d0, d1, nullptr, out,
+          local_row(f.l_idx(), f.l_val(), f.l_pre(), d.wL, P.g.didx, P.g.dval, d0, d1, nullptr, out,
                     d.WL);
       }
     }
     if (INSTR) {
-      f.adjw[x] = (int)(P.g.aoff[id + 1] - P.g.aoff[id]);
-      f.dirw[x] = (int)(P.g.doff[id + 1] - P.g.doff[id]);
+      f.adjw()[x] = (int)(P.g.aoff[id + 1] - P.g.aoff[id]);
+      f.dirw()[x] = (int)(P.g.doff[id + 1] - P.g.doff[id]);
     }
   }
   __syncwarp();
@@ -1437,7 +1455,7 @@ __device__ __forceinline__ void build_frame_L(const Params &P, const Frame &f, c
 __device__ __forceinline__ void clear_map(uint16_t *map, const Frame &f, const Dims &d) {
   if (!map) return;
   BC_LOOP
-  for (int k = lane_id(); k < d.wL; k += 32) map[f.l_idx[k]] = 0xffff;
+  for (int k = lane_id(); k < d.wL; k += 32) map[f.l_idx()[k]] = 0xffff;
   __syncwarp();
 }
 
@@ -1446,12 +1464,12 @@ __device__ __forceinline__ void init_root_sets(const Frame &f, const Dims &d) {
   BC_LOOP
   for (int w = lane; w < d.WR; w += 32) {
     const int rem = d.nR - w * 32;
-    f.setR[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
+    f.setR()[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
   }
   BC_LOOP
   for (int w = lane; w < d.WL; w += 32) {
     const int rem = d.nL - w * 32;
-    f.setL[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
+    f.setL()[w] = rem >= 32 ? FULL : ((1u << rem) - 1u);
   }
   __syncwarp();
 }
@@ -1678,9 +1696,9 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
     carve_ro(f, A.frames + foff, d, sp);
     carve_scratch(f, sc_base, d, p_eff, sp);
     BC_LOOP
-    for (int w = lane; w < d.WR; w += 32) f.setR[(lv - 1) * d.WR + w] = rec[4 + w];
+    for (int w = lane; w < d.WR; w += 32) f.setR()[(lv - 1) * d.WR + w] = rec[4 + w];
     BC_LOOP
-    for (int w = lane; w < d.WL; w += 32) f.setL[(lv - 1) * d.WL + w] = rec[4 + d.WR + w];
+    for (int w = lane; w < d.WL; w += 32) f.setL()[(lv - 1) * d.WL + w] = rec[4 + d.WR + w];
     __syncwarp();
     Acc128 acc{0, 0};
     PH_MARK(0);

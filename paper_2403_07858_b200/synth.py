@@ -281,7 +281,7 @@ def graph_from_torch_csr(u_off, u_idx, v_off, v_idx) -> BipartiteGraph:
 # C5H: C5's base graph with many more planted core triples, so the (8,8) search -- not
 # the level-1 pass -- dominates and one GPU runs for seconds: the multi-GPU scaling
 # workload; calibrated on a B200
-C5H_CORES, C5H_CORE_SEED = 1024, 11
+C5H_CORES, C5H_CORE_SEED = 8192, 11
 
 DEVICE_CONFIGS = {
     "C5": {},

@@ -13,8 +13,8 @@ from paper_2403_07858_b200 import DeviceGraph, EngineConfig, synth  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"
 mode = sys.argv[2] if len(sys.argv) > 2 else "root"
 p, q = synth.CONFIGS[name][1][0]
-if name == "C5":
-    dg = DeviceGraph.from_device_csr(*synth.fr_shaped_csr(device="cuda"))
+if name in synth.DEVICE_CONFIGS:  # C5, C5H: generated on the device
+    dg = DeviceGraph.from_device_csr(*synth.build_device_config(name))
     cap = 1 << 17
 else:
     dg = DeviceGraph(synth.build_config(name))
