@@ -1298,32 +1298,39 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     BC_LOOP
     for (int x = lane; x < d.nL; x += 32) f.lslot()[x] = 0;
     __syncwarp();
-    int *cnt = f.lslot();
+    // two walks with one inlined copy of the walk (instruction cache): pass 0 counts
+    // |N(x) & C_R1| per x into lslot, pass 1 sets the survivors' rowR bits
+    int *lslot = f.lslot();
+    uint32_t *rowR = f.rowR();
+    const int WR = d.WR;
     const int64_t lbase = P.lseg ? P.roff[j] : 0;
-    for_member_hits(P, f, d, f.rids(), map, lbase, [&](int, int lx) { atomicAdd(cnt + lx, 1); });
-    int base = 0;
     BC_LOOP
-    for (int x0 = 0; x0 < d.nL; x0 += 32) {
-      const int x = x0 + lane;
-      const bool sv = x < d.nL && f.lslot()[x] >= P.q_eff;
-      const unsigned m = __ballot_sync(FULL, sv);
-      if (x < d.nL) f.lslot()[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
-      base += __popc(m);
-    }
-    ns1 = base;
-    __syncwarp();
-    if (ROWS && ns1 > 0 && ns1 <= sp.rows(d.nL)) {
-      const int64_t total = (int64_t)ns1 * d.WR;
-      BC_LOOP
-      for (int64_t w = lane; w < total; w += 32) f.rowR()[w] = 0;
-      __syncwarp();
-      uint32_t *rowR = f.rowR();
-      const int *lslot = f.lslot();
-      const int WR = d.WR;
+    for (int pass = 0; pass < 2; pass++) {
       for_member_hits(P, f, d, f.rids(), map, lbase, [&](int i, int lx) {
-        const int sl = lslot[lx];
-        if (sl >= 0) atomicOr(rowR + (sl * WR + (i >> 5)), 1u << (i & 31));
+        if (pass == 0) {
+          atomicAdd(lslot + lx, 1);
+        } else {
+          const int sl = lslot[lx];
+          if (sl >= 0) atomicOr(rowR + (sl * WR + (i >> 5)), 1u << (i & 31));
+        }
       });
+      if (pass == 1) break;
+      int base = 0;
+      BC_LOOP
+      for (int x0 = 0; x0 < d.nL; x0 += 32) {
+        const int x = x0 + lane;
+        const bool sv = x < d.nL && lslot[x] >= P.q_eff;
+        const unsigned m = __ballot_sync(FULL, sv);
+        if (x < d.nL) lslot[x] = sv ? base + __popc(m & lanemask_lt()) : -1;
+        base += __popc(m);
+      }
+      ns1 = base;
+      __syncwarp();
+      if (!(ROWS && ns1 > 0 && ns1 <= sp.rows(d.nL))) break;
+      const int total = ns1 * WR;
+      BC_LOOP
+      for (int w = lane; w < total; w += 32) rowR[w] = 0;
+      __syncwarp();
     }
   } else {
     BC_LOOP
