@@ -277,6 +277,35 @@ __global__ void __launch_bounds__(256) nesting_check(Params P, const Info *__res
 // cursors live in shared memory (one per lane's edge of the current 32-edge round);
 // a row's order is free, so hits take their places by shared-memory atomics.
 // ---------------------------------------------------------------------------
+// Rank-order positions inside each root's directed list (for the restricted rows):
+// keys[i] = rank of dir2 entry i, vals[i] = i; after a per-root sort by rank, the
+// j-th entry of root r's segment is the j-th lowest-ranked member of dir2(r).
+__global__ void dir_rank_keys(const int32_t *__restrict__ didx, const int64_t *__restrict__ rank,
+                              int64_t n, uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (uint32_t)rank[didx[i]];
+  vals[i] = (int32_t)i;
+}
+
+// warp per root: rpos[i] = rank-order position of dir2 entry i inside its root's list,
+// rdir[doff[r] + j] = the j-th lowest-ranked member of dir2(r)
+__global__ void dir_rank_pos(const int64_t *__restrict__ doff, const int32_t *__restrict__ didx,
+                             int64_t n, const int32_t *__restrict__ sorted_vals,
+                             int32_t *__restrict__ rpos, int32_t *__restrict__ rdir) {
+  const int lane = lane_id();
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    const int64_t d0 = doff[r], d1 = doff[r + 1];
+    for (int64_t pidx = d0 + lane; pidx < d1; pidx += 32) {
+      const int32_t i = sorted_vals[pidx];
+      rpos[i] = (int32_t)(pidx - d0);
+      rdir[pidx] = didx[i];
+    }
+  }
+}
+
 struct U32ToI64 {
   __host__ __device__ __forceinline__ int64_t operator()(uint32_t x) const { return (int64_t)x; }
 };
@@ -307,8 +336,9 @@ struct L1Args {
   // entry's row {roffE[e], |R(r, v)|} in lseg
   uint32_t *rcnt;
   const int64_t *__restrict__ roffE;
-  int32_t *rrows;
+  int32_t *rrows;  // entries are rank-order positions in dir2(r) (rpos), not anchor ids
   uint2 *lseg;
+  const int32_t *__restrict__ rpos;  // rank-order position of each dir2 entry
 };
 
 struct RootMap {
@@ -438,7 +468,7 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
           // is free (the walks only count), so a shared-memory atomic places each hit
           if (rr && kd >= 0) {
             const uint32_t at = atomicAdd(runs + os[uu], 1u);
-            if (FILL) A.rrows[at] = ks[uu];
+            if (FILL) A.rrows[at] = __ldg(A.rpos + d0 + kd);
           }
           if (!FILL) {
             if (k >= 0) atomicAdd(col + k, 1ull);
@@ -771,6 +801,117 @@ struct DbgTimer {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Level-1 survivor filter on the restricted rows (p_eff >= 5, wedge-scatter level 1).
+// A task (r, s) has a level-1 R-survivor x iff x is in C_L1 = dir2(r) & dir2(s) and
+// |N(x) & C_R1| >= q (engine.py:331-338).  dir2(s) = {x : |N(x) & N(s)| >= q,
+// rank(x) < rank(s)} (graph.py:192-224, k = q_eff, engine.py:127-135) and C_R1 is a
+// subset of N(s), so for x in dir2(r): x survives iff rank(x) < rank(s) and
+// |N(x) & C_R1| >= q.  The rows R(r, v) hold rank-order positions in dir2(r), so the
+// test is `position < position of s` and the counters are indexed by position: no
+// C_L1 intersection, no slot map, no HTB words.  Counters are u16 pairs in shared
+// memory (a carry into the neighbour only adds false survivors, which the triage
+// kernel re-checks exactly; a count is flagged the moment it reaches q < 2^16).
+// Tasks without a survivor finish here (their level-1 batch is their only work);
+// the others go to the medium list as before.
+// ---------------------------------------------------------------------------
+constexpr int RF_THREADS = 256;
+
+__global__ void __launch_bounds__(RF_THREADS, 4) rfilter_kernel(Params P, EnumArgs A,
+                                                               int budget_words) {
+  extern __shared__ uint32_t smem[];
+  const int lane = lane_id();
+  uint32_t *cnt = smem + (int64_t)(threadIdx.x >> 5) * budget_words;
+  Tally tl;
+  Acc128 total{0, 0, 0};
+  unsigned long long claims = 0;
+  const int q = P.q_eff;
+  BC_LOOP
+  for (;;) {
+    long long qi = 0;
+    if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
+    qi = __shfl_sync(FULL, qi, 0) + A.q0;
+    if (qi >= A.q1) break;
+    claims++;
+    const int j = A.queue[qi];
+    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
+    const int r = P.tasks[t].x;
+    const int64_t d0 = P.dir_off[r];
+    const int rps = P.rpos[d0 + (t - P.troot[r])];  // candidates: positions [0, rps)
+    const Dims d = dims_of(A.info[j]);
+    bool surv = false;
+    if (rps > 2 * budget_words) {
+      surv = true;  // counters do not fit: the triage kernel decides
+    } else if (rps > 0) {
+      BC_LOOP
+      for (int w = lane; w < (rps + 1) / 2; w += 32) cnt[w] = 0;
+      __syncwarp();
+      const int64_t lbase = P.roff[j];
+      BC_LOOP
+      for (int b0 = 0; b0 < d.nR && !surv; b0 += 32) {
+        const int i = b0 + lane;
+        int64_t start = 0;
+        int len = 0;
+        if (i < d.nR) {
+          const uint2 sg = __ldg(P.lseg + lbase + i);
+          start = sg.x;
+          len = (int)sg.y;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int tt = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += tt;
+        }
+        const int excl = incl - len;
+        const int T = __shfl_sync(FULL, incl, 31);
+        constexpr int U = 4;  // gathers in flight per lane
+        BC_LOOP
+        for (int r0 = 0; r0 < T; r0 += 32 * U) {
+          int xs[U];
+#pragma unroll
+          for (int u = 0; u < U; u++) {
+            const int pos = r0 + 32 * u + lane;
+            int sl = 0;  // owning member: the last lane whose exclusive offset is <= pos
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+              const int c = sl + step;
+              const int e = __shfl_sync(FULL, excl, c < 32 ? c : 31);
+              if (c < 32 && e <= pos) sl = c;
+            }
+            const int64_t st = __shfl_sync(FULL, start, sl);
+            const int ex = __shfl_sync(FULL, excl, sl);
+            xs[u] = pos < T ? __ldg(P.rrows + st + (pos - ex)) : INT_MAX;
+          }
+          bool hit = false;
+#pragma unroll
+          for (int u = 0; u < U; u++) {
+            const int x = xs[u];
+            if (x < rps) {
+              const int sh = (x & 1) * 16;
+              const uint32_t old = atomicAdd(cnt + (x >> 1), 1u << sh);
+              hit |= ((old >> sh) & 0xffffu) + 1 >= (uint32_t)q;
+            }
+          }
+          if (__any_sync(FULL, hit)) {
+            surv = true;
+            break;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!surv) {
+      if (lane == 0) tl.batches += node_batches(P, (unsigned)d.nL, d.wR, d.wL, P.p_eff == 3);
+      finish_task(P, Acc128{0, 0, 0}, t, false, total);
+    } else if (lane == 0) {
+      push_heavy(P, A, j, 0);
+    }
+    __syncwarp();
+  }
+  flush_tallies(P, total, tl, claims, 0, false);
+}
+
 int env_int(const char *name, int dflt) {  // development knobs
   const char *v = getenv(name);
   return v && *v ? atoi(v) : dflt;
@@ -902,6 +1043,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.lists = nullptr;
   P.lseg = nullptr;
   P.rrows = nullptr;
+  P.rdir = nullptr;
+  P.rpos = nullptr;
+  P.dir_off = nullptr;
+  P.troot = nullptr;
   P.rowR_mode = (cfg.flags & BC_FLAG_ROWR_SCATTER) ? 1 : (cfg.flags & BC_FLAG_ROWR_PROBE) ? 2 : 0;
   if (P.rowR_mode == 0) P.rowR_mode = env_int("BC_ROWS_MODE", 0);  // development A/B
   // slot map over anchor words for rowL (u16 per word) when it is small
@@ -934,6 +1079,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     DBuf<int64_t> rr_off;
     DBuf<int32_t> rr_rows;
     DBuf<uint2> rr_seg;
+    DBuf<int32_t> rr_rpos, rr_rdir;  // rank-order positions / dir2 lists in rank order
     int l1_mode = (cfg.flags & BC_FLAG_L1_SCATTER) ? 1 : (cfg.flags & BC_FLAG_L1_PROBE) ? 2 : 0;
     if (l1_mode == 0) l1_mode = env_int("BC_L1_MODE", 0);  // development A/B
     if (l1_mode == 0) {
@@ -1017,6 +1163,33 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
         rr_cnt.alloc(n_anchor_edges, st);
         rr_cnt.zero();
         A1.rcnt = rr_cnt.p;
+        // rank-order positions: restricted rows hold them, so a task (r, s) finds the
+        // candidates x with rank(x) < rank(s) by comparing positions (rfilter_kernel)
+        const int64_t D = s.dir2_pairs;
+        rr_rpos.alloc(D, st);
+        rr_rdir.alloc(D, st);
+        {
+          DBuf<uint32_t> k0, k1;
+          DBuf<int32_t> v0, v1;
+          k0.alloc(D, st);
+          k1.alloc(D, st);
+          v0.alloc(D, st);
+          v1.alloc(D, st);
+          dir_rank_keys<<<(unsigned)((D + 255) / 256 + 1), 256, 0, st>>>(s.dir_idx.p, s.rank.p, D,
+                                                                        k0.p, v0.p);
+          size_t tmp = 0;
+          BC_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, k0.p, k1.p, v0.p, v1.p, D, n,
+                                                      s.dir_off.p, s.dir_off.p + 1, st));
+          DBuf<char> tb;
+          tb.alloc(tmp, st);
+          BC_CUDA(cub::DeviceSegmentedSort::SortPairs(tb.p, tmp, k0.p, k1.p, v0.p, v1.p, D, n,
+                                                      s.dir_off.p, s.dir_off.p + 1, st));
+          dir_rank_pos<<<sms * 8, 256, 0, st>>>(s.dir_off.p, s.dir_idx.p, n, v1.p, rr_rpos.p,
+                                                rr_rdir.p);
+          BC_CHECK_LAUNCH();
+          launches += 3;
+        }
+        A1.rpos = rr_rpos.p;
       }
       const int l1w = L1_THREADS / 32;
       const size_t l1smem = (size_t)l1w * (A1.map_words + (A1.map_words + 1) / 2 + 32) * 4;
@@ -1100,6 +1273,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       if (A1.rcnt) {
         P.lseg = rr_seg.p;
         P.rrows = rr_rows.p;
+        P.rdir = rr_rdir.p;
+        P.rpos = rr_rpos.p;
+        P.dir_off = s.dir_off.p;
+        P.troot = s.troot.p;
       }
       if (getenv("BC_DEBUG")) {
         BC_CUDA(cudaStreamSynchronize(st));
@@ -1355,8 +1532,24 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
               BC_CUDA(cudaMemsetAsync(ctr.p + CTR_HEAVY, 0, 8, st));
               dt.mark("pre-filter");
-              if (compact) filter_launch_c1((unsigned)fblocks, fsmem, st, P, F);
-              else filter_launch_c0((unsigned)fblocks, fsmem, st, P, F);
+              if (P.lseg && s.q_eff < 65536) {
+                // restricted rows: the rank-position filter (no frames, no slot map)
+                const int rbudget = 1024;  // words per warp: 2048 u16 counters
+                const size_t rsmem = (size_t)(RF_THREADS / 32) * rbudget * 4;
+                BC_CUDA(cudaFuncSetAttribute(rfilter_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)rsmem));
+                int per_sm = 0;
+                BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rfilter_kernel,
+                                                                      RF_THREADS, rsmem));
+                rfilter_kernel<<<(unsigned)(sms * std::max(per_sm, 1)), RF_THREADS, rsmem, st>>>(
+                    P, F, rbudget);
+                BC_CHECK_LAUNCH();
+              } else if (compact) {
+                filter_launch_c1((unsigned)fblocks, fsmem, st, P, F);
+              } else {
+                filter_launch_c0((unsigned)fblocks, fsmem, st, P, F);
+              }
               dt.mark("filter");
               unsigned long long hm = 0;
               copy_d2h(&hm, ctr.p + CTR_HEAVY, sizeof hm, st);

@@ -103,7 +103,11 @@ struct Params {
   // member v = lists[i] and lseg[i] = {start, len} of R(r, v) = N(v) & dir2(r) in rrows
   // (or null: the wedge walks read the whole rows N(v))
   const uint2 *__restrict__ lseg;
-  const int32_t *__restrict__ rrows;
+  const int32_t *__restrict__ rrows;   // R(r, v) entries: rank-order positions in dir2(r)
+  const int32_t *__restrict__ rdir;    // dir2(r) in rank order at dir_off[r] (position -> id)
+  const int32_t *__restrict__ rpos;    // dir2 entry (id order) -> its rank-order position
+  const int64_t *__restrict__ dir_off; // plain dir2 list offsets
+  const int64_t *__restrict__ troot;   // first task of each root
 };
 
 // global task id of this shard's local task j
@@ -1185,7 +1189,7 @@ __device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int 
 template <typename F>
 __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f, const Dims &d,
                                                 const int *members, const uint16_t *map,
-                                                int64_t lbase, F fn) {
+                                                int64_t lbase, int64_t rbase, F fn) {
   const int lane = lane_id();
   const int32_t *__restrict__ src = P.lseg ? P.rrows : P.g.bidx;
   BC_LOOP
@@ -1230,6 +1234,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
         const int ex = __shfl_sync(FULL, excl, sl);
         own[u] = sl;
         xs[u] = pos < T ? __ldg(src + st + (pos - ex)) : -1;
+        if (P.lseg && xs[u] >= 0) xs[u] = __ldg(P.rdir + rbase + xs[u]);  // position -> id
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -1304,9 +1309,10 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     uint32_t *rowR = f.rowR();
     const int WR = d.WR;
     const int64_t lbase = P.lseg ? P.roff[j] : 0;
+    const int64_t rbase = P.lseg ? P.dir_off[r] : 0;
     BC_LOOP
     for (int pass = 0; pass < 2; pass++) {
-      for_member_hits(P, f, d, f.rids(), map, lbase, [&](int i, int lx) {
+      for_member_hits(P, f, d, f.rids(), map, lbase, rbase, [&](int i, int lx) {
         if (pass == 0) {
           atomicAdd(lslot + lx, 1);
         } else {
