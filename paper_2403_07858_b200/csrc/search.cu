@@ -339,6 +339,7 @@ struct L1Args {
   int32_t *rrows;  // entries are rank-order positions in dir2(r) (rpos), not anchor ids
   uint2 *lseg;
   const int32_t *__restrict__ rpos;  // rank-order position of each dir2 entry
+  int cur_words;  // pass 2: shared-memory list cursors per warp (0: global cursors)
 };
 
 struct RootMap {
@@ -385,10 +386,11 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
   const int wib = threadIdx.x >> 5;
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int mw = A.map_words;
-  uint32_t *wsm = sm + (int64_t)wib * (mw + (mw + 1) / 2 + 32);
+  uint32_t *wsm = sm + (int64_t)wib * (mw + (mw + 1) / 2 + 32 + (FILL ? A.cur_words : 0));
   uint32_t *bits = mw ? wsm : nullptr;
   uint16_t *pre = mw ? (uint16_t *)(bits + mw) : nullptr;
   uint32_t *runs = wsm + mw + (mw + 1) / 2;  // R(r, v) cursor of the round's edge base + lane
+  uint32_t *ccur = runs + 32;  // pass 2: the unit's list cursors (u32) when they fit
   const bool rr = A.rcnt != nullptr;
   if (bits)
     for (int i = lane; i < mw; i += 32) bits[i] = 0;
@@ -404,7 +406,16 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
     RootMap m{bits, pre, A.didx + d0, (int)(A.doff[r + 1] - d0)};
     rootmap_set(m, true);
     const int64_t T0 = A.troot[r];
+    const int t0mod = A.nshards > 1 ? (int)(T0 % A.nshards) : 0;  // 32-bit shard test per hit
     unsigned long long *col = A.aux + A.ubase[r] + (int64_t)c * m.D;
+    // the unit's cursors in shared memory: the per-hit cursor read is then an LDS, not a
+    // dependent global load (list offsets fit u32 when cur_words > 0)
+    const bool scur = FILL && m.D <= A.cur_words;
+    if (scur) {
+      BC_LOOP
+      for (int i = lane; i < m.D; i += 32) ccur[i] = (uint32_t)col[i];
+      __syncwarp();
+    }
     const int64_t e0 = A.aoff[r] + (int64_t)c * L1_CH;
     const int64_t e1 = min(A.aoff[r + 1], e0 + L1_CH);
     // the rows of 32 neighbours at a time as one flattened list over the lanes; rounds of
@@ -463,7 +474,7 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
         for (int uu = 0; uu < U; uu++) {
           const int kd = ks[uu] >= 0 ? m.slot(ks[uu]) : -1;  // s in dir2(r)
           int k = kd;
-          if (k >= 0 && (T0 + k) % A.nshards != A.shard) k = -1;
+          if (k >= 0 && A.nshards > 1 && (t0mod + k) % A.nshards != A.shard) k = -1;
           // R(r, v) of every local edge holds all of dir2(r), whatever the shard; its order
           // is free (the walks only count), so a shared-memory atomic places each hit
           if (rr && kd >= 0) {
@@ -475,13 +486,16 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
           } else {
             // same-slot hits of this round, ranked by lane (= by ascending v)
             const unsigned grp = __match_any_sync(FULL, k >= 0 ? k : -1 - lane);
-            const unsigned long long c0 = k >= 0 ? col[k] : 0ull;
+            const unsigned long long c0 = k < 0 ? 0ull : scur ? (unsigned long long)ccur[k] : col[k];
             __syncwarp();
             if (k >= 0) {
               const unsigned long long at = c0 + __popc(grp & lanemask_lt());
               A.lists[at] = vs[uu];
               if (rr) A.lseg[at] = make_uint2(rss[uu], rls[uu]);
-              if (((grp >> lane) >> 1) == 0) col[k] = c0 + __popc(grp);
+              if (((grp >> lane) >> 1) == 0) {
+                if (scur) ccur[k] = (uint32_t)(c0 + __popc(grp));
+                else col[k] = c0 + __popc(grp);
+              }
             }
             __syncwarp();
           }
@@ -1263,8 +1277,19 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           s.dir_off.p, l1_roff.p, aux.p);
       A1.lists = l1_lists.p;
       A1.next = nxt.p + 1;
+#ifndef L1_CUR_WORDS
+#define L1_CUR_WORDS 512
+#endif
+      A1.cur_words = n_entries < (int64_t(1) << 32) ? (int)std::min<unsigned long long>(maxD, L1_CUR_WORDS) : 0;
+      const size_t l1smem2 = l1smem + (size_t)l1w * A1.cur_words * 4;
+      BC_CUDA(cudaFuncSetAttribute(l1_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)l1smem2));
+      int per_sm2 = 0;
+      BC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, l1_scatter<true>, L1_THREADS,
+                                                            l1smem2));
+      const int64_t l1blocks2 = (int64_t)sms * std::max(per_sm2, 1);
       dt.mark("l1 offsets");
-      l1_scatter<true><<<(unsigned)l1blocks, L1_THREADS, l1smem, st>>>(A1);
+      l1_scatter<true><<<(unsigned)l1blocks2, L1_THREADS, l1smem2, st>>>(A1);
       BC_CHECK_LAUNCH();
       dt.mark("l1 fill");
       launches += 12;
