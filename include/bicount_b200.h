@@ -89,6 +89,9 @@ typedef struct bc_config {
                                    violation */
 #define BC_FLAG_FULL_ROWS 1024  /* wedge-scatter frames walk whole opposite-layer rows N(v)
                                    instead of the root-restricted rows N(v) & dir2(r) (tests) */
+#define BC_FLAG_FORCE_TRIAGE 2048 /* p_eff >= 5: run the survivor filter + triage path even
+                                     when every task's frame would fit the split arena (it is
+                                     chosen by size otherwise: C5-scale task counts; tests) */
 
 /* CountReport (engine.py:64-79) plus device measurements. */
 typedef struct bc_report {

@@ -18,7 +18,7 @@ ABI_VERSION = 3
 BC_FLAG_TASK_COUNTS, BC_FLAG_INSTRUMENT, BC_FLAG_NO_SPLIT = 1, 2, 4
 BC_FLAG_L1_SCATTER, BC_FLAG_L1_PROBE, BC_FLAG_ROWR_SCATTER, BC_FLAG_ROWR_PROBE = 8, 16, 32, 64
 BC_FLAG_TASK_SHARD, BC_FLAG_TRACK_TASKS, BC_FLAG_CHECK_NESTING = 128, 256, 512
-BC_FLAG_FULL_ROWS = 1024
+BC_FLAG_FULL_ROWS, BC_FLAG_FORCE_TRIAGE = 1024, 2048
 
 (BC_X_UND_SIZE, BC_X_RANK, BC_X_ORDER, BC_X_DIR_OFF, BC_X_DIR_IDX, BC_X_HADJ_OFF,
  BC_X_HADJ_IDX, BC_X_HADJ_VAL, BC_X_HDIR_OFF, BC_X_HDIR_IDX, BC_X_HDIR_VAL, BC_X_TASKS,

@@ -780,10 +780,6 @@ __global__ void max_reduce(const int64_t *a, int64_t n, unsigned long long *out)
   if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
 }
 
-inline int64_t env_i64(const char *name, int64_t dflt) {  // development A/B knobs
-  const char *e = getenv(name);
-  return e ? atoll(e) : dflt;
-}
 
 inline unsigned blocks_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
@@ -806,7 +802,7 @@ void build_htb(const int64_t *off, const int32_t *idx, int64_t n, int64_t E, DBu
   words.zero();
   DBuf<int32_t> flag, wpos;
   // small families keep the per-row kernels (fewer launches); large ones go flat
-  const int64_t flat_min = env_i64("BC_HTB_FLAT_MIN", int64_t(1) << 17);
+  const int64_t flat_min = int64_t(1) << 17;
   const bool flat = E >= flat_min && E < (int64_t(1) << 31) - 1;
   if (flat) {  // word slots by one scan over the entries
     DBuf<uint8_t> rs;
@@ -1026,7 +1022,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     L++;
     // light anchors (small wedge pools) go to the warp-per-vertex kernel, the rest keep
     // the LPT order of the block kernel
-    const bool use_light = !wide && getenv("BC_TH_NOLIGHT") == nullptr;
+    const bool use_light = !wide;
     const bool select = use_light || slice;
     int64_t n_light = 0, n_heavy = n;
     DBuf<int64_t> nsel;
@@ -1062,7 +1058,6 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     cap = std::max<int64_t>(cap, 1);
     // touched-word lists when a vertex's pool is small against the tile's words
     bool summary = (double)hb[1] / (double)n < (double)((tile + 31) / 32);
-    if (const char *e = getenv("BC_TH_SUMMARY")) summary = atoi(e) != 0;  // development A/B
     auto kern = wide ? (summary ? twohop_kernel<true, true> : twohop_kernel<true, false>)
                      : (summary ? twohop_kernel<false, true> : twohop_kernel<false, false>);
     BC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1275,8 +1270,7 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     unsigned long long h[DENSE_NT];
     copy_d2h(h, hist.p, sizeof h, st);
     BC_CUDA(cudaStreamSynchronize(st));
-    const char *db = getenv("BC_DENSE_MB");  // development A/B
-    const int64_t budget = int64_t(db ? atoi(db) : 64) << 20;  // bytes of dense rows (L2-sized)
+    const int64_t budget = int64_t(64) << 20;  // bytes of dense rows (L2-sized)
     int pick = -1;
     for (int t = 0; t < DENSE_NT; t++) {
       const int64_t T = int64_t(16) << t;

@@ -510,28 +510,6 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
   }
 }
 
-// development check: |N(r) & N(s)| by merge, thread per local task
-__global__ void l1_naive(const int2 *__restrict__ tasks, const int64_t *ltask, int64_t nloc,
-                         int shard, int nshards,
-                         const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
-                         const int64_t *__restrict__ cnt, unsigned long long *bad) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= nloc) return;
-  const int2 tk = tasks[task_id(ltask, shard, nshards, j)];
-  int64_t a = aoff[tk.x], a1 = aoff[tk.x + 1], b = aoff[tk.y], b1 = aoff[tk.y + 1], c = 0;
-  while (a < a1 && b < b1) {
-    const int x = aidx[a], y = aidx[b];
-    c += x == y;
-    a += x <= y;
-    b += y <= x;
-  }
-  if (c != cnt[j]) {
-    const unsigned long long k = atomicAdd(bad, 1ull);
-    if (k < 5) printf("l1 check: task %lld (%d,%d) naive %lld pass1 %lld\n", (long long)j, tk.x, tk.y,
-                      (long long)c, (long long)cnt[j]);
-  }
-}
-
 // per local task: |C_R1| = sum over its root's chunks (pass-1 columns)
 __global__ void l1_task_totals(const int2 *__restrict__ tasks, const int64_t *ltask, int64_t nloc,
                                int shard, int nshards,
@@ -926,10 +904,6 @@ __global__ void __launch_bounds__(RF_THREADS, 4) rfilter_kernel(Params P, EnumAr
   flush_tallies(P, total, tl, claims, 0, false);
 }
 
-int env_int(const char *name, int dflt) {  // development knobs
-  const char *v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 template <typename K, typename V>
 void sort_pairs_desc(const K *kin, K *kout, const V *vin, V *vout, int64_t n, cudaStream_t st) {
@@ -1062,7 +1036,6 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.dir_off = nullptr;
   P.troot = nullptr;
   P.rowR_mode = (cfg.flags & BC_FLAG_ROWR_SCATTER) ? 1 : (cfg.flags & BC_FLAG_ROWR_PROBE) ? 2 : 0;
-  if (P.rowR_mode == 0) P.rowR_mode = env_int("BC_ROWS_MODE", 0);  // development A/B
   // slot map over anchor words for rowL (u16 per word) when it is small
   const int64_t anchor_words = (s.n + 31) / 32;
   P.map_words = (s.p_eff >= 4 && anchor_words <= 4096) ? (int)((anchor_words + 1) & ~1) : 0;
@@ -1095,7 +1068,6 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     DBuf<uint2> rr_seg;
     DBuf<int32_t> rr_rpos, rr_rdir;  // rank-order positions / dir2 lists in rank order
     int l1_mode = (cfg.flags & BC_FLAG_L1_SCATTER) ? 1 : (cfg.flags & BC_FLAG_L1_PROBE) ? 2 : 0;
-    if (l1_mode == 0) l1_mode = env_int("BC_L1_MODE", 0);  // development A/B
     if (l1_mode == 0) {
       DBuf<unsigned long long> c2;
       c2.alloc(2, st);
@@ -1225,18 +1197,6 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       l1_task_totals<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(
           s.tasks.p, ltask.p, nloc, shard, nshards, s.troot.p, ubase.p, unit_first.p,
           s.dir_off.p, aux.p, cnt.p);
-      if (getenv("BC_CHECK_L1")) {
-        DBuf<unsigned long long> bad;
-        bad.alloc(1, st);
-        bad.zero();
-        l1_naive<<<(unsigned)((nloc + 255) / 256), 256, 0, st>>>(s.tasks.p, ltask.p, nloc, shard,
-                                                                 nshards,
-                                                                 s.aoff, s.aidx, cnt.p, bad.p);
-        unsigned long long hb = 0;
-        copy_d2h(&hb, bad.p, 8, st);
-        BC_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "[bc level1] check: %llu of %lld task counts differ\n", hb, (long long)nloc);
-      }
       l1_roff.alloc(nloc + 1, st);
       scan_excl(cnt.p, l1_roff.p, nloc + 1, st);
       int64_t n_entries = 0;
@@ -1334,63 +1294,6 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       BC_CUDA(cudaStreamSynchronize(st));
       n_alive = (int64_t)h[CTR_ALIVE];
       const int64_t max_ro = (int64_t)h[CTR_MAXRO], max_scr = (int64_t)h[CTR_MAXSCR];
-      if (const char *dump = getenv("BC_DUMP_L1")) {  // development: Info + C_R1 lists
-        std::vector<Info> hi(nloc);
-        copy_d2h(hi.data(), info.p, nloc * sizeof(Info), st);
-        std::vector<int64_t> ro;
-        std::vector<int32_t> li;
-        if (P.lists) {
-          ro.resize(nloc + 1);
-          copy_d2h(ro.data(), P.roff, (nloc + 1) * 8, st);
-          BC_CUDA(cudaStreamSynchronize(st));
-          li.resize(ro[nloc]);
-          copy_d2h(li.data(), P.lists, ro[nloc] * 4, st);
-        }
-        BC_CUDA(cudaStreamSynchronize(st));
-        if (FILE *fh = fopen(dump, "wb")) {
-          int64_t n = nloc, nl = (int64_t)li.size();
-          fwrite(&n, 8, 1, fh);
-          fwrite(hi.data(), sizeof(Info), nloc, fh);
-          fwrite(&nl, 8, 1, fh);
-          if (nl) {
-            fwrite(ro.data(), 8, nloc + 1, fh);
-            fwrite(li.data(), 4, nl, fh);
-          }
-          fclose(fh);
-        }
-      }
-      if (getenv("BC_LEVEL1_STATS")) {  // development: level-1 shape of the workload
-        std::vector<Info> hi(nloc);
-        copy_d2h(hi.data(), info.p, nloc * sizeof(Info), st);
-        BC_CUDA(cudaStreamSynchronize(st));
-        std::vector<int> crs, cls;
-        double sum_lr = 0, sum_rowR = 0;
-        for (const Info &x : hi)
-          if (x.cl >= s.p_eff - 2 && x.cr >= s.q_eff) {
-            crs.push_back(x.cr);
-            cls.push_back(x.cl);
-            sum_lr += (double)x.cl * x.cr;
-            sum_rowR += (double)x.cl * ((x.cr + 31) / 32);
-          }
-        std::sort(crs.begin(), crs.end());
-        std::sort(cls.begin(), cls.end());
-        auto pct = [](const std::vector<int> &v, double f) {
-          return v.empty() ? 0 : v[std::min(v.size() - 1, (size_t)(f * v.size()))];
-        };
-        float l1ms = 0;
-        BC_CUDA(cudaEventRecord(e1, st));
-        BC_CUDA(cudaEventSynchronize(e1));
-        BC_CUDA(cudaEventElapsedTime(&l1ms, e0, e1));
-        fprintf(stderr,
-                "[bc level1] tasks %lld alive %lld  level1 %.3f ms  max_ro %lld max_scr %lld words\n"
-                "  |C_R1| p50 %d p90 %d p99 %d max %d   |C_L1| p50 %d p90 %d p99 %d max %d\n"
-                "  sum |C_L1||C_R1| %.4g  sum rowR words %.4g\n",
-                (long long)nloc, (long long)n_alive, l1ms, (long long)max_ro, (long long)max_scr,
-                pct(crs, .5), pct(crs, .9), pct(crs, .99), crs.empty() ? 0 : crs.back(),
-                pct(cls, .5), pct(cls, .9), pct(cls, .99), cls.empty() ? 0 : cls.back(), sum_lr,
-                sum_rowR);
-        if (getenv("BC_LEVEL1_ONLY")) n_alive = 0;
-      }
       if (n_alive > 0) {
         // pre-runtime LPT order: alive tasks by |C_L1|*|C_R1| descending
         DBuf<int32_t> ids, queue;
@@ -1440,7 +1343,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
         if (!split) {
           // whole tasks per warp; frames in shared memory
           const bool lazy = s.p_eff == 4 && !has_rowL(s.p_eff, P.map_words);
-          const int budget = env_int("BC_ENUM_BUDGET", 1200);
+          const int budget = 1200;  // frame words per warp (measured optimum on C2, p_eff = 4)
           const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
           const EnumVariant ev{instr, lazy, false, false};
           const int64_t blocks = (int64_t)sms * eblocks(ev, smem);
@@ -1464,8 +1367,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           DBuf<int32_t> heavy, heavy_ns1, hq, hcap;
           // triage only when splitting everything would not fit one frame arena
           // (millions of mostly light tasks, e.g. C5); C3/C4-sized queues split all
-          int T = env_int("BC_TRIAGE", 16);
-          if (T > 0 && !env_int("BC_TRIAGE_FORCE", 0)) {
+          int T = 16;  // level-1 survivors a triaged task may have before it is split
+          if (!(cfg.flags & BC_FLAG_FORCE_TRIAGE)) {
             DBuf<int64_t> ro_all, sub_all, sum;
             ro_all.alloc(n_alive, st);
             sub_all.alloc(n_alive, st);
@@ -1486,7 +1389,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             if (frames_total <= (int64_t(1) << 28) && n_alive <= (int64_t(1) << 18)) T = 0;
           }
           if (T > 0) {
-            const int budget = env_int("BC_TRIAGE_BUDGET", 1024);
+            const int budget = 1024;
             const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
             const EnumVariant ev{instr, false, false, true};
             const int64_t blocks = (int64_t)sms * eblocks(ev, smem);
@@ -1498,7 +1401,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             // triage drains the alive tasks in emission order: the tasks of one root are
             // adjacent, so their C_R1 members' rows (all in N(root)) are re-read from L2
             DBuf<int32_t> tq;
-            if (!env_int("BC_TRIAGE_LPT", 0)) {
+            {
               DBuf<int32_t> ids;
               DBuf<uint8_t> flags;
               DBuf<int64_t> nsel;
@@ -1520,7 +1423,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             }
             B.budget_words = budget;
             B.triage = T;
-            B.triage_work = env_int("BC_TRIAGE_WORK", 1 << 16);
+            B.triage_work = 1 << 16;  // expansion budget before a task is deferred
             B.heavy = heavy.p;
             B.heavy_ns1 = heavy_ns1.p;
             DBuf<uint32_t> gs;
@@ -1634,8 +1537,8 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
             // writes every frame to the frame arena and pushes the split-level nodes,
             // then sub_kernel drains them heaviest first with every warp.
-            const int split_level = env_int("BC_SPLIT_LEVEL", s.p_eff <= 6 ? 2 : 3);
-            const int budget = env_int("BC_SPLIT_BUDGET", 1024);
+            const int split_level = s.p_eff <= 6 ? 2 : 3;
+            const int budget = 1024;
             const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
             const EnumVariant ev{instr, false, true, false};
             const size_t ssmem = (size_t)wpb * (budget + LEAF_WORDS) * 4;

@@ -1111,6 +1111,7 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
         // the children's children are leaf-parents: expand every child at once
         work += expand_children<INSTR>(P, f, d, level, lb, acc, tl);
         if (work > limit) return false;
+        __syncwarp();  // every lane's read of ns[li0] above precedes lane 0's write
         if (lane == 0) f.ns()[li0] = 0;
         __syncwarp();
       }

@@ -48,6 +48,7 @@ class EngineConfig:
     level1: str = "auto"      # "scatter" (root-grouped wedge walk) | "probe" (per-task HTB)
     rows: str = "auto"        # candidate rows: "scatter" | "probe"
     restricted_rows: bool = True  # scatter walks read N(v) & dir2(root), not all of N(v)
+    force_triage: bool = False    # p_eff >= 5: filter + triage path whatever the task count
     shard_mode: str = "root"  # multi-GPU: whole roots, degree-balanced | "task" interleave
 
     def validate(self) -> None:
@@ -163,6 +164,8 @@ def _make_config(cfg: EngineConfig, anchor: str, rank, roots, shard=(0, 1), flag
                 "probe": _abi.BC_FLAG_ROWR_PROBE}[cfg.rows]
     if not cfg.restricted_rows:
         c.flags |= _abi.BC_FLAG_FULL_ROWS
+    if cfg.force_triage:
+        c.flags |= _abi.BC_FLAG_FORCE_TRIAGE
     if cfg.shard_mode == "task":
         c.flags |= _abi.BC_FLAG_TASK_SHARD
     keep = []

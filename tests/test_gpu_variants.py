@@ -281,3 +281,52 @@ def test_assemble_upper_device_matches_host():
         off2, ids2 = assemble_upper(sl)
         assert torch.equal(off, off2) and torch.equal(ids, ids2)
     dg.close()
+
+
+# The survivor filter + triage path (chosen by size for C5-scale task counts) forced on
+# small graphs, with the root-restricted rows (rank-position filter) and with whole
+# opposite-layer rows: exact counts, per-task counts, batches and shard sums.
+TRIAGE_PATHS = [dict(force_triage=True),
+                dict(force_triage=True, restricted_rows=False),
+                dict(force_triage=True, level1="scatter", rows="scatter"),
+                dict(force_triage=True, level1="probe", rows="scatter"),
+                dict(force_triage=True, level1="scatter", rows="probe"),
+                dict(restricted_rows=False)]
+
+
+@pytest.mark.parametrize("kw", TRIAGE_PATHS)
+def test_forced_triage_paths_random_deep(kw):
+    rng = np.random.default_rng(29)
+    for i in range(9):
+        nu, nv = int(rng.integers(40, 100)), int(rng.integers(40, 100))
+        g = synth.random_bipartite(nu, nv, float(rng.uniform(0.15, 0.4)), int(rng.integers(1 << 30)))
+        p, q = int(rng.integers(5, 9)), int(rng.integers(2, 6))
+        anchor = ["auto", "U", "V"][i % 3]
+        want = O.count(g, p, q, anchor=anchor, per_task=True)
+        dg = DeviceGraph(g)
+        try:
+            cfg = EngineConfig(anchor=anchor, **kw)
+            rep, per_task = dg.count_raw(p, q, cfg, task_counts=True)
+            got = int(rep.count_lo) | (int(rep.count_hi) << 64)
+            assert got == want.count, (i, p, q, kw)
+            assert per_task == want.task_counts, (i, p, q, kw)
+            assert rep.batches_executed == want.batches_executed, (i, p, q, kw)
+            assert rep.tasks_emitted == want.tasks_emitted
+            total = 0
+            for k in range(3):
+                r, _ = dg.count_raw(p, q, cfg, shard=(k, 3))
+                total += int(r.count_lo) | (int(r.count_hi) << 64)
+            assert total == want.count, (i, p, q, kw)
+        finally:
+            dg.close()
+
+
+@pytest.mark.parametrize("name,p,q", [("C3", 6, 3), ("C4", 8, 8)])
+@pytest.mark.parametrize("kw", TRIAGE_PATHS[:2])
+def test_forced_triage_configs(golden, name, p, q, kw):
+    g = synth.build_config(name)
+    want = golden["configs"][name][f"({p},{q})"]["hybrid"]
+    rep = count_bicliques(g, p, q, EngineConfig(**kw))
+    assert str(rep.count) == want["count"]
+    assert rep.batches_executed == want["batches"]
+    assert rep.tasks_emitted == want["emitted"]
