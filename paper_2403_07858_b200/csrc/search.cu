@@ -290,14 +290,15 @@ __global__ void dir_rank_keys(const int32_t *__restrict__ didx, const int64_t *_
 
 // warp per root: rpos[i] = rank-order position of dir2 entry i inside its root's list,
 // rdir[doff[r] + j] = the j-th lowest-ranked member of dir2(r)
-__global__ void dir_rank_pos(const int64_t *__restrict__ doff, const int32_t *__restrict__ didx,
-                             int64_t n, const int32_t *__restrict__ sorted_vals,
+__global__ void dir_rank_pos(const int64_t *__restrict__ doff, const int64_t *__restrict__ dend,
+                             const int32_t *__restrict__ didx, int64_t n,
+                             const int32_t *__restrict__ sorted_vals,
                              int32_t *__restrict__ rpos, int32_t *__restrict__ rdir) {
   const int lane = lane_id();
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = gw; r < n; r += nw) {
-    const int64_t d0 = doff[r], d1 = doff[r + 1];
+    const int64_t d0 = doff[r], d1 = dend[r];  // roots this rank does not walk: empty
     for (int64_t pidx = d0 + lane; pidx < d1; pidx += 32) {
       const int32_t i = sorted_vals[pidx];
       rpos[i] = (int32_t)(pidx - d0);
@@ -340,6 +341,7 @@ struct L1Args {
   uint2 *lseg;
   const int32_t *__restrict__ rpos;  // rank-order position of each dir2 entry
   int cur_words;  // pass 2: shared-memory list cursors per warp (0: global cursors)
+  const int64_t *__restrict__ rebase;  // per root: first index of its edges in rcnt / roffE
 };
 
 struct RootMap {
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
     // 32 consecutive positions keep the owners (hence v) ascending across the lanes
     for (int64_t base = e0; base < e1; base += 32) {
       const int64_t e = base + lane;
+      const int64_t el = rr ? A.rebase[r] + (e - A.aoff[r]) : 0;  // this rank's edge index
       int32_t v = 0;
       int64_t st = 0;
       int len = 0;
@@ -431,8 +434,8 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
         st = __ldg(A.boff + v);
         len = (int)(__ldg(A.boff + v + 1) - st);
         if (rr && FILL) {
-          rs = (uint32_t)A.roffE[e];
-          rl = (uint32_t)(A.roffE[e + 1] - A.roffE[e]);
+          rs = (uint32_t)A.roffE[el];
+          rl = (uint32_t)(A.roffE[el + 1] - A.roffE[el]);
         }
       }
       if (rr) runs[lane] = rs;
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
         }
       }
       __syncwarp();
-      if (rr && !FILL && e < e1) A.rcnt[e] = runs[lane];
+      if (rr && !FILL && e < e1) A.rcnt[el] = runs[lane];
       __syncwarp();
     }
     __syncwarp();  // lanes still probing the map must finish before it is cleared
@@ -551,20 +554,31 @@ __global__ void l1_cursors(const int2 *__restrict__ tasks, const int64_t *ltask,
 // per root: chunks (units) and aux block size (0 for roots without tasks)
 __global__ void l1_root_sizes(const int64_t *__restrict__ aoff, const int64_t *__restrict__ doff,
                               const int64_t *__restrict__ troot, int64_t n, int32_t *__restrict__ nunits,
-                              int64_t *__restrict__ auxw, const int32_t *__restrict__ owner,
-                              int shard) {
+                              int64_t *__restrict__ auxw, int64_t *__restrict__ redges,
+                              const int32_t *__restrict__ owner, int shard) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n) return;
   int32_t nu = 0;
-  int64_t w = 0;
+  int64_t w = 0, de = 0;
   const int64_t D = doff[r + 1] - doff[r];
   if (troot[r] >= 0 && D > 0 && (!owner || owner[r] == shard)) {
     const int64_t deg = aoff[r + 1] - aoff[r];
     nu = (int32_t)((deg + L1_CH - 1) / L1_CH);
     w = (int64_t)nu * D;
+    de = deg;
   }
   nunits[r] = nu;
   auxw[r] = w;
+  redges[r] = de;  // edges this rank walks: restricted rows are indexed by them only
+}
+
+// dir2 segments of the roots this rank walks (others empty): the rank-position sort
+// covers only those
+__global__ void l1_owned_segments(const int64_t *__restrict__ doff, const int32_t *__restrict__ nunits,
+                                  int64_t n, int64_t *__restrict__ seg_end) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  seg_end[r] = nunits[r] > 0 ? doff[r + 1] : doff[r];
 }
 
 __global__ void l1_unit_roots(const int32_t *__restrict__ unit_first, int64_t n,
@@ -1063,6 +1077,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     DBuf<int64_t> l1_roff;
     DBuf<int32_t> l1_lists;
     DBuf<uint32_t> rr_cnt;  // root-restricted rows (l1_scatter)
+    DBuf<int64_t> rr_ebase;
     DBuf<int64_t> rr_off;
     DBuf<int32_t> rr_rows;
     DBuf<uint2> rr_seg;
@@ -1093,17 +1108,21 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     if (l1_mode == 1) {
       const int64_t n = s.n;
       DBuf<int32_t> nunits, unit_first, unit_root;
-      DBuf<int64_t> auxw, ubase;
+      DBuf<int64_t> auxw, ubase, redges;
       nunits.alloc(n + 1, st);
       auxw.alloc(n + 1, st);
+      redges.alloc(n + 1, st);
       nunits.zero();
       auxw.zero();
+      redges.zero();
       l1_root_sizes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-          s.aoff, s.dir_off.p, s.troot.p, n, nunits.p, auxw.p, owner.p, shard);
+          s.aoff, s.dir_off.p, s.troot.p, n, nunits.p, auxw.p, redges.p, owner.p, shard);
       unit_first.alloc(n + 1, st);
       ubase.alloc(n + 1, st);
+      rr_ebase.alloc(n + 1, st);
       scan_excl(nunits.p, unit_first.p, n + 1, st);
       scan_excl(auxw.p, ubase.p, n + 1, st);
+      scan_excl(redges.p, rr_ebase.p, n + 1, st);
       DBuf<unsigned long long> mx;
       mx.alloc(1, st);
       mx.zero();
@@ -1142,10 +1161,11 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       // root-restricted rows for the compact frames' wedge walks (slot map needed, p_eff >= 4)
       const bool want_rr = s.p_eff >= 4 && (s.n + 31) / 32 <= 4096 &&
                            !(cfg.flags & BC_FLAG_FULL_ROWS);
-      int64_t n_anchor_edges = 0;
+      int64_t n_anchor_edges = 0;  // edges of the roots this rank walks
       if (want_rr) {
-        copy_d2h(&n_anchor_edges, s.aoff + n, sizeof n_anchor_edges, st);
+        copy_d2h(&n_anchor_edges, rr_ebase.p + n, sizeof n_anchor_edges, st);
         BC_CUDA(cudaStreamSynchronize(st));
+        A1.rebase = rr_ebase.p;
         rr_cnt.alloc(n_anchor_edges, st);
         rr_cnt.zero();
         A1.rcnt = rr_cnt.p;
@@ -1163,15 +1183,19 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           v1.alloc(D, st);
           dir_rank_keys<<<(unsigned)((D + 255) / 256 + 1), 256, 0, st>>>(s.dir_idx.p, s.rank.p, D,
                                                                         k0.p, v0.p);
+          DBuf<int64_t> seg_end;
+          seg_end.alloc(n, st);
+          l1_owned_segments<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.dir_off.p, nunits.p, n,
+                                                                        seg_end.p);
           size_t tmp = 0;
           BC_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, k0.p, k1.p, v0.p, v1.p, D, n,
-                                                      s.dir_off.p, s.dir_off.p + 1, st));
+                                                      s.dir_off.p, seg_end.p, st));
           DBuf<char> tb;
           tb.alloc(tmp, st);
           BC_CUDA(cub::DeviceSegmentedSort::SortPairs(tb.p, tmp, k0.p, k1.p, v0.p, v1.p, D, n,
-                                                      s.dir_off.p, s.dir_off.p + 1, st));
-          dir_rank_pos<<<sms * 8, 256, 0, st>>>(s.dir_off.p, s.dir_idx.p, n, v1.p, rr_rpos.p,
-                                                rr_rdir.p);
+                                                      s.dir_off.p, seg_end.p, st));
+          dir_rank_pos<<<sms * 8, 256, 0, st>>>(s.dir_off.p, seg_end.p, s.dir_idx.p, n, v1.p,
+                                                rr_rpos.p, rr_rdir.p);
           BC_CHECK_LAUNCH();
           launches += 3;
         }
