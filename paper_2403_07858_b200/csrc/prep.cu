@@ -284,6 +284,24 @@ __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__
   if (lane == 0 && ptot) atomicAdd(out + 1, ptot);
 }
 
+// Output bound of the anchors one rank owns (sharded preprocessing): the same
+// sum_u min(n - 1, pool(u) / k) over the selected light and heavy ids only, so a rank
+// allocates its slice's share, not the whole graph's 2-hop output.
+__global__ void owned_bound(const int32_t *__restrict__ ids_a, int64_t na,
+                            const int32_t *__restrict__ ids_b, int64_t nb,
+                            const int32_t *__restrict__ pool_of, int64_t n, uint32_t k,
+                            unsigned long long *out) {
+  unsigned long long tot = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na + nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = i < na ? ids_a[i] : ids_b[i - na];
+    const unsigned long long b = (unsigned long long)pool_of[u] / k;
+    tot += b < (unsigned long long)(n - 1) ? b : (unsigned long long)(n - 1);
+  }
+  tot = warp_sum(tot);
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(out, tot);
+}
+
 // Light anchors (pool <= LIGHT_POOL wedges, most vertices of a power-law graph) skip
 // the block kernel's tile counters and its ~10 block barriers per vertex: one warp
 // gathers the vertex's upper wedge ids (w > u) into shared memory, bitonic-sorts them,
@@ -1054,6 +1072,19 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       n_heavy = hn[1];
     }
     BC_CUDA(cudaStreamSynchronize(st));
+    if (slice) {  // size the output by the owned anchors only
+      DBuf<unsigned long long> ob;
+      ob.alloc(1, st);
+      ob.zero();
+      owned_bound<<<sms * 4, 256, 0, st>>>(light_ids.p, n_light, heavy_ids.p, n_heavy, pool_of.p,
+                                           n, k, ob.p);
+      BC_CHECK_LAUNCH();
+      L++;
+      unsigned long long hob = 0;
+      copy_d2h(&hob, ob.p, sizeof hob, st);
+      BC_CUDA(cudaStreamSynchronize(st));
+      hb[0] = hob;
+    }
     int64_t cap = std::min<int64_t>((int64_t)hb[0], int64_t(1) << 31);
     cap = std::max<int64_t>(cap, 1);
     // touched-word lists when a vertex's pool is small against the tile's words

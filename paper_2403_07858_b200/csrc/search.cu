@@ -119,8 +119,16 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
         const int i = b + lane;
         bool start = false;
         if (i < cr) {
-          const uint32_t w = (uint32_t)__ldg(P.lists + l0 + i) >> 5;
-          start = i == 0 || ((uint32_t)__ldg(P.lists + l0 + i - 1) >> 5) != w;
+          uint32_t w, wp = 0;
+          if (P.roffE) {  // edge-indexed list: member ids through the anchor CSR
+            const int64_t ab = P.csr_aoff[tk.x] - P.rebase[tk.x];
+            w = (uint32_t)__ldg(P.csr_aidx + ab + __ldg(P.lists + l0 + i)) >> 5;
+            if (i > 0) wp = (uint32_t)__ldg(P.csr_aidx + ab + __ldg(P.lists + l0 + i - 1)) >> 5;
+          } else {
+            w = (uint32_t)__ldg(P.lists + l0 + i) >> 5;
+            if (i > 0) wp = (uint32_t)__ldg(P.lists + l0 + i - 1) >> 5;
+          }
+          start = i == 0 || wp != w;
         }
         wr += __popc(__ballot_sync(FULL, start));
       }
@@ -332,13 +340,11 @@ struct L1Args {
   int32_t *lists;           // pass 2
   unsigned long long *next;
   // root-restricted rows R(r, v) = N(v) & dir2(r) for every edge e = (r, v) of a unit
-  // (null: not built).  Pass 1 counts |R(r, v)| into rcnt[e]; pass 2 writes the rows
-  // at roffE[e] (ascending ids) and, beside each C_R1 list entry v of task (r, s), the
-  // entry's row {roffE[e], |R(r, v)|} in lseg
+  // (null: not built).  Pass 1 counts |R(r, v)| into rcnt[e]; pass 2 writes the rows at
+  // roffE[e] and, as the C_R1 list entry of task (r, s), the edge index e instead of v
   uint32_t *rcnt;
   const int64_t *__restrict__ roffE;
   int32_t *rrows;  // entries are rank-order positions in dir2(r) (rpos), not anchor ids
-  uint2 *lseg;
   const int32_t *__restrict__ rpos;  // rank-order position of each dir2 entry
   int cur_words;  // pass 2: shared-memory list cursors per warp (0: global cursors)
   const int64_t *__restrict__ rebase;  // per root: first index of its edges in rcnt / roffE
@@ -428,15 +434,12 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
       int32_t v = 0;
       int64_t st = 0;
       int len = 0;
-      uint32_t rs = 0, rl = 0;  // this lane's edge: R(r, v) start and length (pass 2)
+      uint32_t rs = 0;  // this lane's edge: R(r, v) start (pass 2)
       if (e < e1) {
         v = __ldg(A.aidx + e);
         st = __ldg(A.boff + v);
         len = (int)(__ldg(A.boff + v + 1) - st);
-        if (rr && FILL) {
-          rs = (uint32_t)A.roffE[el];
-          rl = (uint32_t)(A.roffE[el + 1] - A.roffE[el]);
-        }
+        if (rr && FILL) rs = (uint32_t)A.roffE[el];
       }
       if (rr) runs[lane] = rs;
       __syncwarp();
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
       for (int r0 = 0; r0 < T; r0 += 32 * U) {
         int ks[U], os[U];
         int32_t vs[U];
-        uint32_t rss[U], rls[U];
+        int32_t els[U];
 #pragma unroll
         for (int uu = 0; uu < U; uu++) {
           const int pos = r0 + 32 * uu + lane;
@@ -467,10 +470,7 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
           const int eo = __shfl_sync(FULL, excl, sl);
           vs[uu] = __shfl_sync(FULL, v, sl);
           os[uu] = sl;
-          if (FILL && rr) {
-            rss[uu] = __shfl_sync(FULL, rs, sl);
-            rls[uu] = __shfl_sync(FULL, rl, sl);
-          }
+          if (FILL && rr) els[uu] = __shfl_sync(FULL, (int32_t)el, sl);
           ks[uu] = pos < T ? __ldg(A.bidx + so + (pos - eo)) : -1;
         }
 #pragma unroll
@@ -493,8 +493,9 @@ __global__ void __launch_bounds__(L1_THREADS) l1_scatter(L1Args A) {
             __syncwarp();
             if (k >= 0) {
               const unsigned long long at = c0 + __popc(grp & lanemask_lt());
-              A.lists[at] = vs[uu];
-              if (rr) A.lseg[at] = make_uint2(rss[uu], rls[uu]);
+              // with restricted rows the entry is the edge (r, v): its member id and its row
+              // R(r, v) both follow from it, one 4-byte scattered write per entry
+              A.lists[at] = rr ? els[uu] : vs[uu];
               if (((grp >> lane) >> 1) == 0) {
                 if (scur) ccur[k] = (uint32_t)(c0 + __popc(grp));
                 else col[k] = c0 + __popc(grp);
@@ -635,7 +636,7 @@ __global__ void l1_pool(const int64_t *__restrict__ aoff, const int32_t *__restr
 // members' degrees (wedge scatter) vs 2 * |C_L1| * words(C_R1) (probes)
 __global__ void rows_cost(const Info *__restrict__ info, int64_t nloc, int stride,
                           const int64_t *__restrict__ roff, const int32_t *__restrict__ lists,
-                          const int64_t *__restrict__ boff, const uint2 *__restrict__ lseg,
+                          const int64_t *__restrict__ boff, const int64_t *__restrict__ roffE,
                           int p_eff, int q, unsigned long long *out) {
   const int lane = lane_id();
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -645,8 +646,9 @@ __global__ void rows_cost(const Info *__restrict__ info, int64_t nloc, int strid
     const Info in = info[j];
     if (in.cr < q || in.cl < p_eff - 2) continue;
     for (int64_t i = roff[j] + lane; i < roff[j + 1]; i += 32) {
-      if (lseg) {  // the walk reads the root-restricted row R(r, v)
-        sc += lseg[i].y;
+      if (roffE) {  // the walk reads the root-restricted row R(r, v)
+        const int64_t e = lists[i];
+        sc += (unsigned long long)(roffE[e + 1] - roffE[e]);
       } else {
         const int v = lists[i];
         sc += (unsigned long long)(boff[v + 1] - boff[v]);
@@ -859,9 +861,9 @@ __global__ void __launch_bounds__(RF_THREADS, 4) rfilter_kernel(Params P, EnumAr
         int64_t start = 0;
         int len = 0;
         if (i < d.nR) {
-          const uint2 sg = __ldg(P.lseg + lbase + i);
-          start = sg.x;
-          len = (int)sg.y;
+          const int64_t e = __ldg(P.lists + lbase + i);
+          start = __ldg(P.roffE + e);
+          len = (int)(__ldg(P.roffE + e + 1) - start);
         }
         int incl = len;
 #pragma unroll
@@ -1043,7 +1045,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
   P.claims = want_claims ? claims.p : nullptr;
   P.roff = nullptr;
   P.lists = nullptr;
-  P.lseg = nullptr;
+  P.roffE = nullptr;
+  P.rebase = nullptr;
+  P.csr_aoff = nullptr;
+  P.csr_aidx = nullptr;
   P.rrows = nullptr;
   P.rdir = nullptr;
   P.rpos = nullptr;
@@ -1080,7 +1085,6 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     DBuf<int64_t> rr_ebase;
     DBuf<int64_t> rr_off;
     DBuf<int32_t> rr_rows;
-    DBuf<uint2> rr_seg;
     DBuf<int32_t> rr_rpos, rr_rdir;  // rank-order positions / dir2 lists in rank order
     int l1_mode = (cfg.flags & BC_FLAG_L1_SCATTER) ? 1 : (cfg.flags & BC_FLAG_L1_PROBE) ? 2 : 0;
     if (l1_mode == 0) {
@@ -1244,12 +1248,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
         copy_d2h(&rr_total, rr_off.p + E, sizeof rr_total, st);
         BC_CUDA(cudaStreamSynchronize(st));
         launches += 2;
-        if (rr_total < (int64_t(1) << 32)) {
+        if (rr_total < (int64_t(1) << 32) && E < (int64_t(1) << 31)) {
           rr_rows.alloc(rr_total, st);
-          rr_seg.alloc(n_entries, st);
           A1.roffE = rr_off.p;
           A1.rrows = rr_rows.p;
-          A1.lseg = rr_seg.p;
           if (getenv("BC_DEBUG"))
             fprintf(stderr, "[bc level1] restricted rows: %lld entries\n", (long long)rr_total);
         } else {
@@ -1280,7 +1282,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       P.roff = l1_roff.p;
       P.lists = l1_lists.p;
       if (A1.rcnt) {
-        P.lseg = rr_seg.p;
+        P.roffE = rr_off.p;
+        P.rebase = rr_ebase.p;
+        P.csr_aoff = s.aoff;
+        P.csr_aidx = s.aidx;
         P.rrows = rr_rows.p;
         P.rdir = rr_rdir.p;
         P.rpos = rr_rpos.p;
@@ -1344,7 +1349,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
             rc.zero();
             const int stride = nloc > (int64_t(1) << 20) ? 16 : 1;
             rows_cost<<<(unsigned)std::min<int64_t>((nloc / stride * 32 + 255) / 256 + 1, sms * 16), 256,
-                        0, st>>>(info.p, nloc, stride, P.roff, P.lists, s.boff, P.lseg, s.p_eff,
+                        0, st>>>(info.p, nloc, stride, P.roff, P.lists, s.boff, P.roffE, s.p_eff,
                                  s.q_eff, rc.p);
             unsigned long long hc[2];
             copy_d2h(hc, rc.p, sizeof hc, st);
@@ -1484,7 +1489,7 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
               BC_CUDA(cudaMemsetAsync(ctr.p + CTR_NEXT, 0, 8, st));
               BC_CUDA(cudaMemsetAsync(ctr.p + CTR_HEAVY, 0, 8, st));
               dt.mark("pre-filter");
-              if (P.lseg && s.q_eff < 65536) {
+              if (P.roffE && s.q_eff < 65536) {
                 // restricted rows: the rank-position filter (no frames, no slot map)
                 const int rbudget = 1024;  // words per warp: 2048 u16 counters
                 const size_t rsmem = (size_t)(RF_THREADS / 32) * rbudget * 4;

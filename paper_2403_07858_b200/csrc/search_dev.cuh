@@ -99,10 +99,14 @@ struct Params {
   const int64_t *__restrict__ ltask;    // root sharding: global id of local task j (or null:
                                         //   task interleave t = shard + j * nshards)
   unsigned *claims;                     // optional [n_tasks]: claims per task (track_tasks)
-  // root-restricted rows (wedge-scatter level 1): C_R1 list entry i of task (r, s) holds
-  // member v = lists[i] and lseg[i] = {start, len} of R(r, v) = N(v) & dir2(r) in rrows
-  // (or null: the wedge walks read the whole rows N(v))
-  const uint2 *__restrict__ lseg;
+  // root-restricted rows (wedge-scatter level 1; roffE null: not built, lists hold ids and
+  // the wedge walks read the whole rows N(v)).  With them, C_R1 list entry i of task (r, s)
+  // is the rank-local index e of the edge (r, v): v = csr_aidx[csr_aoff[r] - rebase[r] + e]
+  // and R(r, v) = N(v) & dir2(r) is rrows[roffE[e], roffE[e + 1])
+  const int64_t *__restrict__ roffE;
+  const int64_t *__restrict__ rebase;   // per root: its first edge index
+  const int64_t *__restrict__ csr_aoff; // anchor -> opposite CSR (work graph)
+  const int32_t *__restrict__ csr_aidx;
   const int32_t *__restrict__ rrows;   // R(r, v) entries: rank-order positions in dir2(r)
   const int32_t *__restrict__ rdir;    // dir2(r) in rank order at dir_off[r] (position -> id)
   const int32_t *__restrict__ rpos;    // dir2 entry (id order) -> its rank-order position
@@ -1143,7 +1147,7 @@ __device__ __forceinline__ bool dfs(const Params &P, const Frame &f, const Dims 
 
 // Sorted id list -> HTB words (htb.py:89-115) with exclusive prefix
 // popcounts (o_pre[words] = n); returns the word count.
-__device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int n,
+__device__ __forceinline__ int list_to_htb(const int32_t *ids, int n,
                                            uint32_t *o_idx, uint32_t *o_val, int *o_pre) {
   const int lane = lane_id();
   int pos = 0;
@@ -1153,15 +1157,15 @@ __device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int 
     uint32_t word = 0;
     bool start = false;
     if (i < n) {
-      word = (uint32_t)__ldg(ids + i) >> 5;
-      start = i == 0 || ((uint32_t)__ldg(ids + i - 1) >> 5) != word;
+      word = (uint32_t)ids[i] >> 5;
+      start = i == 0 || ((uint32_t)ids[i - 1] >> 5) != word;
     }
     const unsigned m = __ballot_sync(FULL, start);
     if (start) {
       uint32_t v = 0;
       BC_LOOP
       for (int k = i; k < n; k++) {
-        const uint32_t id = (uint32_t)__ldg(ids + k);
+        const uint32_t id = (uint32_t)ids[k];
         if ((id >> 5) != word) break;
         v |= 1u << (id & 31);
       }
@@ -1184,7 +1188,7 @@ __device__ __forceinline__ int list_to_htb(const int32_t *__restrict__ ids, int 
 // rows are.  Work is sum_{v in C_R1} deg(v), read as contiguous rows, instead
 // of |C_L1| probes of (possibly hub-sized) adjacency rows.
 //
-// With root-restricted rows (P.lseg), member i's row is R(r, v) = N(v) & dir2(r)
+// With root-restricted rows (P.roffE), member i's row is R(r, v) = N(v) & dir2(r)
 // (list entry lbase + i): every x of C_L1 = dir2(r) & dir2(s) in N(v) is in it, so the
 // hits are the same and the walk is shorter.
 template <typename F>
@@ -1192,17 +1196,17 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
                                                 const int *members, const uint16_t *map,
                                                 int64_t lbase, int64_t rbase, F fn) {
   const int lane = lane_id();
-  const int32_t *__restrict__ src = P.lseg ? P.rrows : P.g.bidx;
+  const int32_t *__restrict__ src = P.roffE ? P.rrows : P.g.bidx;
   BC_LOOP
   for (int b0 = 0; b0 < d.nR; b0 += 32) {
     const int i = b0 + lane;
     int64_t start = 0;
     int len = 0;
     if (i < d.nR) {
-      if (P.lseg) {
-        const uint2 sg = __ldg(P.lseg + lbase + i);
-        start = sg.x;
-        len = (int)sg.y;
+      if (P.roffE) {
+        const int64_t e = __ldg(P.lists + lbase + i);
+        start = __ldg(P.roffE + e);
+        len = (int)(__ldg(P.roffE + e + 1) - start);
       } else {
         const int v = members[i];
         start = __ldg(P.g.boff + v);
@@ -1235,7 +1239,7 @@ __device__ __forceinline__ void for_member_hits(const Params &P, const Frame &f,
         const int ex = __shfl_sync(FULL, excl, sl);
         own[u] = sl;
         xs[u] = pos < T ? __ldg(src + st + (pos - ex)) : -1;
-        if (P.lseg && xs[u] >= 0) xs[u] = __ldg(P.rdir + rbase + xs[u]);  // position -> id
+        if (P.roffE && xs[u] >= 0) xs[u] = __ldg(P.rdir + rbase + xs[u]);  // position -> id
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -1266,8 +1270,19 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
                                              uint16_t *map, PhaseClock &ph_) {
   const int lane = lane_id();
   int card;
-  if (P.lists) list_to_htb(P.lists + P.roff[j], d.nR, f.r_idx(), f.r_val(), f.r_pre());
-  else isect_adj<true>(P.g, r, s, card, f.r_idx(), f.r_val(), f.r_pre());
+  if (P.lists && P.roffE && sp.compact) {
+    // edge-indexed list: members into rids (ascending: edges of r follow its sorted row),
+    // then their HTB words
+    const int64_t l0 = P.roff[j], abase = P.csr_aoff[r] - P.rebase[r];
+    BC_LOOP
+    for (int i = lane; i < d.nR; i += 32) f.rids()[i] = __ldg(P.csr_aidx + abase + __ldg(P.lists + l0 + i));
+    __syncwarp();
+    list_to_htb(f.rids(), d.nR, f.r_idx(), f.r_val(), f.r_pre());
+  } else if (P.lists && !P.roffE) {
+    list_to_htb(P.lists + P.roff[j], d.nR, f.r_idx(), f.r_val(), f.r_pre());
+  } else {
+    isect_adj<true>(P.g, r, s, card, f.r_idx(), f.r_val(), f.r_pre());
+  }
   isect_dir<true>(P.g, r, s, card, f.l_idx(), f.l_val(), f.l_pre());
   PH_MARK(1);
   // decode C_L1 ids (ascending, htb.py:42-52); fill the slot map
@@ -1284,7 +1299,7 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
         v &= v - 1;
       }
   }
-  if (sp.compact) {  // C_R1 members, ascending
+  if (sp.compact && !(P.lists && P.roffE)) {  // C_R1 members, ascending
     BC_LOOP
     for (int k = lane; k < d.wR; k += 32) {
       uint32_t v = f.r_val()[k];
@@ -1309,8 +1324,8 @@ __device__ __forceinline__ int build_frame_R(const Params &P, const Frame &f, co
     int *lslot = f.lslot();
     uint32_t *rowR = f.rowR();
     const int WR = d.WR;
-    const int64_t lbase = P.lseg ? P.roff[j] : 0;
-    const int64_t rbase = P.lseg ? P.dir_off[r] : 0;
+    const int64_t lbase = P.roffE ? P.roff[j] : 0;
+    const int64_t rbase = P.roffE ? P.dir_off[r] : 0;
     BC_LOOP
     for (int pass = 0; pass < 2; pass++) {
       for_member_hits(P, f, d, f.rids(), map, lbase, rbase, [&](int i, int lx) {
