@@ -60,3 +60,21 @@ def test_c5_shards_sum_to_total(c5):
         parts += int(r.count_lo) | (int(r.count_hi) << 64)
     assert parts == total
     assert rep.tasks_emitted == 18900520
+
+
+def test_c5_full_total_matches_chunked_oracle(c5):
+    """The whole C5 (8,8) count and the reference's counters against the full offline
+    CPU oracle run (tests/golden/c5_full.json, 44 root chunks summed by
+    scripts/c5_full_oracle.py, the decomposition of engine.py:155-162)."""
+    import json
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c5_full.json")))
+    _, dg = c5
+    rep, _ = dg.count_raw(8, 8, EngineConfig(batch_buffer_capacity=CAP))
+    assert (int(rep.count_lo) | (int(rep.count_hi) << 64)) == int(gold["count"])
+    assert rep.tasks_emitted == gold["tasks_emitted"]
+    assert rep.roots_filtered == gold["roots_filtered"]
+    assert rep.batches_executed == gold["batches_executed"]
+    ins, _ = dg.count_raw(8, 8, EngineConfig(batch_buffer_capacity=CAP, instrument=True))
+    assert ins.intersections == gold["intersections"]
+    assert ins.operand_words == gold["operand_words"]
