@@ -103,6 +103,9 @@ struct DevStructs {
   // 2-hop slice (sharded preprocessing): upper-list lengths of every anchor (0 unless
   // owned) and the owned anchors' upper ids in vertex order
   DBuf<int32_t> slice_lens, slice_ids;
+  // wedge pool sum_{v in N(u)} deg(v) per anchor (saturated at 2^31 - 1) when the 2-hop
+  // construction ran here (null when the upper lists were injected)
+  DBuf<int32_t> pool;
   int64_t slice_n_ids = -1;
 };
 

@@ -261,8 +261,18 @@ __global__ void __launch_bounds__(TH_THREADS) twohop_kernel(
 
 // upper bound on the 2-hop output: per anchor u, the kept ids (multiplicity >= k)
 // number at most min(n - 1, pool(u) / k), pool(u) = sum_{v in N(u)} deg(v)
+// opposite-layer degrees as int32 (an L2-resident gather table: C5's 8.96 M opposite
+// vertices are 36 MB, against 72 MB of int64 offsets read twice per wedge)
+__global__ void opp_degrees(const int64_t *__restrict__ boff, int64_t m, int32_t *__restrict__ deg) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v < m) {
+    const int64_t d = boff[v + 1] - boff[v];
+    deg[v] = d < INT32_MAX ? (int32_t)d : INT32_MAX;
+  }
+}
+
 __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
-                             const int64_t *__restrict__ boff, int64_t n, uint32_t k,
+                             const int32_t *__restrict__ bdeg, int64_t n, uint32_t k,
                              unsigned long long *out, int32_t *__restrict__ pool_of) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -270,10 +280,8 @@ __global__ void twohop_bound(const int64_t *__restrict__ aoff, const int32_t *__
   unsigned long long tot = 0, ptot = 0;
   for (int64_t u = gw; u < n; u += nw) {
     unsigned long long pool = 0;
-    for (int64_t e = aoff[u] + lane; e < aoff[u + 1]; e += 32) {
-      const int v = aidx[e];
-      pool += (unsigned long long)(boff[v + 1] - boff[v]);
-    }
+    for (int64_t e = aoff[u] + lane; e < aoff[u + 1]; e += 32)
+      pool += (unsigned long long)__ldg(bdeg + __ldg(aidx + e));
     pool = warp_sum(pool);
     if (lane == 0) pool_of[u] = pool < 0x7fffffffull ? (int32_t)pool : 0x7fffffff;
     const unsigned long long b = pool / k;
@@ -1032,10 +1040,17 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
     ctrs.alloc(2, st);
     used.alloc(2, st);
     used.zero();
-    DBuf<int32_t> pool_of, light_ids, heavy_ids;
+    DBuf<int32_t> light_ids, heavy_ids;
+    DBuf<int32_t> &pool_of = s.pool;  // kept: level 1 sums it for its mode choice
     pool_of.alloc(n, st);
-    twohop_bound<<<warp_blocks(n, sms), 256, 0, st>>>(s.aoff, s.aidx, s.boff, n, k, used.p,
-                                                      pool_of.p);
+    {
+      DBuf<int32_t> bdeg;
+      bdeg.alloc(s.m, st);
+      opp_degrees<<<blocks_for(s.m, 256), 256, 0, st>>>(s.boff, s.m, bdeg.p);
+      twohop_bound<<<warp_blocks(n, sms), 256, 0, st>>>(s.aoff, s.aidx, bdeg.p, n, k, used.p,
+                                                        pool_of.p);
+      L++;
+    }
     BC_CHECK_LAUNCH();
     L++;
     // light anchors (small wedge pools) go to the warp-per-vertex kernel, the rest keep

@@ -612,6 +612,16 @@ __global__ void l1_probe_cost(const int2 *__restrict__ tasks, const int64_t *lta
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+__global__ void l1_pool_sum(const int32_t *__restrict__ pool, const int64_t *__restrict__ troot,
+                            int64_t n, unsigned long long *out, const int32_t *__restrict__ owner,
+                            int shard) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long c = 0;
+  if (r < n && troot[r] >= 0 && (!owner || owner[r] == shard)) c = (unsigned long long)pool[r];
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 __global__ void l1_pool(const int64_t *__restrict__ aoff, const int32_t *__restrict__ aidx,
                         const int64_t *__restrict__ boff, const int64_t *__restrict__ troot,
                         int64_t n, unsigned long long *out, const int32_t *__restrict__ owner,
@@ -1093,8 +1103,13 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
       c2.zero();
       l1_probe_cost<<<sms * 8, 256, 0, st>>>(s.tasks.p, ltask.p, nloc, shard, nshards,
                                              s.hadj_off.p, c2.p);
-      l1_pool<<<sms * 8, 256, 0, st>>>(s.aoff, s.aidx, s.boff, s.troot.p, s.n, c2.p + 1,
-                                       owner.p, shard);
+      if (s.pool.p) {  // the pools the 2-hop construction measured
+        l1_pool_sum<<<(unsigned)((s.n + 255) / 256), 256, 0, st>>>(s.pool.p, s.troot.p, s.n,
+                                                                  c2.p + 1, owner.p, shard);
+      } else {
+        l1_pool<<<sms * 8, 256, 0, st>>>(s.aoff, s.aidx, s.boff, s.troot.p, s.n, c2.p + 1,
+                                         owner.p, shard);
+      }
       BC_CHECK_LAUNCH();
       unsigned long long hc[2];
       copy_d2h(hc, c2.p, sizeof hc, st);
