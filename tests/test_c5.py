@@ -1,9 +1,12 @@
-"""FR-shaped config C5 (SURVEY 8(c) config-5 parity): a full CPU count is hours,
-so parity is pinned by (i) the exact count of sampled roots -- planted-core roots,
-where the (8,8) bicliques live, plus seeded random roots -- against the CPU oracle
-run on the same full graph (reference rank, reference task order), and (ii) equal
-totals over task shards (the multi-GPU decomposition).  The graph is generated on
-the GPU by the integer counter-based recipe (synth.fr_shaped_csr)."""
+"""FR-shaped config C5 (SURVEY 8(c) config-5 parity).  A full CPU count is hours, so
+(i) the whole total and the reference's counters are pinned by one offline chunked
+oracle run (tests/golden/c5_full.json, scripts/c5_full_oracle.py: 3.1 h on 6 threads),
+(ii) sampled roots -- planted-core roots, where the (8,8) bicliques live, plus seeded
+random roots -- are re-counted by the CPU oracle on the same full graph in the test
+(reference rank, reference task order), and (iii) task shards (the multi-GPU
+decomposition) sum to the total.  The graph is generated on the GPU by the integer
+counter-based recipe (synth.fr_shaped_csr), bit-identical to the CPU recipe the
+offline run used."""
 
 import os
 
