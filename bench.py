@@ -281,14 +281,17 @@ def pq_of(args):
 
 def compulsory_bytes(r, m: int, e: int) -> int:
     """Bytes the enumeration kernels must read at least once (each input once, no
-    re-reads): the level-1 facts (16 B/task) and LPT queue (4 B/alive task), the C_R1
-    lists of the wedge-scatter level 1 (4 B/entry), the opposite-layer CSR the candidate
-    rows are built from (8 B/row offset + 4 B/id), the directed 2-hop HTB (8 B/word),
-    and the adjacency HTB (8 B/word) when level 1 probes instead of scattering."""
-    b = 16 * r.tasks_consumed + 4 * r.tasks_alive + 4 * r.level1_entries
-    b += 8 * (m + 1) + 4 * e + 8 * r.dir2_words
-    if r.level1_entries == 0:
-        b += 8 * r.adj_words
+    re-reads): the tasks (8 B), their level-1 facts (16 B) and the LPT queue (4 B/alive
+    task); with the wedge-scatter level 1 the C_R1 lists (4 B/entry, edge indices) and
+    the root-restricted rows they point to (4 B/entry rows + 8 B/edge row offsets + 4 B/edge
+    member ids + 8 B/dir2 pair rank positions and rank-ordered lists), else the
+    adjacency HTB (8 B/word) the level-1 sets are re-intersected from; always the
+    directed 2-hop HTB (8 B/word) C_L1 comes from."""
+    b = 24 * r.tasks_consumed + 4 * r.tasks_alive + 8 * r.dir2_words
+    if r.level1_entries > 0:
+        b += 4 * r.level1_entries + 4 * r.level1_entries + 12 * e + 8 * r.dir2_pairs
+    else:
+        b += 8 * r.adj_words + 8 * (m + 1) + 4 * e
     return int(b)
 
 
@@ -478,8 +481,9 @@ def main():
                           "enum": 1e3 * statistics.mean(enum_s)},
             "roofline": {
                 "bound": "hbm",
-                "kernel": "enumeration kernels of one step (filter_kernel, enum_kernel "
-                          "triage/split/whole-task launches, sub_kernel), the dominant phase",
+                "kernel": "enumeration kernels of one step (rfilter_kernel / filter_kernel, "
+                          "enum_kernel triage/split/whole-task launches, sub_kernel), the "
+                          "dominant phase",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None,
                 "traffic": dram,
@@ -488,8 +492,9 @@ def main():
                 "traffic_source": tr_src,
                 "algorithmic_bytes": comp,
                 "algorithmic": "compulsory bytes: every input the enumeration kernels read, "
-                               "once (level-1 facts, queue, C_R1 lists, opposite-layer CSR, "
-                               "dir2 HTB); traffic / algorithmic = re-read factor",
+                               "once (tasks, level-1 facts, queue, C_R1 edge lists, restricted "
+                               "rows + offsets + member ids, rank positions, dir2 HTB); "
+                               "traffic / algorithmic = re-read factor",
                 "algorithmic_frac": comp / t_enum / 1e9 / peak if t_enum > 0 else None,
                 "l2_bytes": tr["l2_bytes"] if tr else None,
                 "l2_gbs": tr["l2_bytes"] / t_enum / 1e9 if tr and t_enum > 0 else None,
