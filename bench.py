@@ -58,6 +58,7 @@ CAPACITY = {"C5": 1 << 17, "C5H": 1 << 17}
 # roots, extrapolated by task share (a full CPU count is hours; tests/golden/c5_full.json
 # holds the one full offline run)
 SAMPLE_FRAC = {"C5": 0.002, "C5H": 0.002}
+STRATA = 22  # root-id ranges the sample is stratified over
 FALLBACK_HBM = 6650.0
 ENUM_KERNELS = ("enum_kernel", "sub_kernel", "filter_kernel")
 
@@ -178,6 +179,27 @@ def traffic_for(workload: str):
     return t, t.get("source", "profiles/r2/traffic.json")
 
 
+CAL_CHUNK = {"C5": (11000, 12000)}  # calibration chunk of the offline full CPU run
+
+
+def calibration_chunk(config: str):
+    """(lo, hi, chunk seconds, full-run seconds, chunks, threads) of the offline full CPU
+    oracle run of this config (profiles/r2/c5_oracle_chunks.jsonl), or None."""
+    span = CAL_CHUNK.get(config)
+    if span is None:
+        return None
+    try:
+        rows = [json.loads(x) for x in open(os.path.join(ROOT, "profiles", "r2",
+                                                         "c5_oracle_chunks.jsonl")) if x.strip()]
+    except (OSError, ValueError):
+        return None
+    full = sum(r["seconds"] for r in rows)
+    hit = [r for r in rows if (r["lo"], r["hi"]) == span]
+    if not hit or sum(r["hi"] - r["lo"] for r in rows) != rows[0]["n_roots_total"]:
+        return None
+    return span[0], span[1], hit[0]["seconds"], full, len(rows), hit[0]["threads"]
+
+
 def sample_roots(prep, frac: float, seed: int):
     """A seeded sample of anchor roots and its share of the emitted tasks."""
     import numpy as np
@@ -209,14 +231,52 @@ def cpu_oracle_run(g, p, q, threads: int, config: str, seed: int = 1, prep_cache
         cache["prep"] = O.Prepared(g, p, q, threads=threads)
         cache["t_prep"] = time.perf_counter() - t0
     prep, t_prep = cache["prep"], cache["t_prep"]
-    roots, share = sample_roots(prep, frac, seed)
-    t1 = time.perf_counter()
-    O.count(g, p, q, workers=threads, threads=threads, capacity=cap, roots=roots, prepared=prep)
-    t_cnt = time.perf_counter() - t1
-    est = t_prep + t_cnt / max(share, 1e-12)
-    return None, est, (f"full CPU preprocessing ({t_prep:.1f} s) + counting {len(roots)} seeded "
-                       f"random roots ({100 * share:.3f}% of tasks, {t_cnt:.1f} s), "
-                       f"extrapolated by task share")
+    cal = calibration_chunk(config)
+    if cal is not None:
+        # a fixed chunk of roots of the offline full CPU run, scaled by that chunk's share of
+        # the full run's time: per-root cost is heavy-tailed (planted cores), so random root
+        # samples extrapolate with a spread of 7x; the chunk ratio is measured, not assumed
+        lo, hi, t_off, t_full, n_chunks, thr = cal
+        import numpy as np
+
+        t1 = time.perf_counter()
+        O.count(g, p, q, workers=threads, threads=threads, capacity=cap,
+                roots=np.arange(lo, hi), prepared=prep)
+        dt = time.perf_counter() - t1
+        est = t_prep + dt * t_full / t_off
+        return None, est, (f"full CPU preprocessing ({t_prep:.1f} s) + counting roots "
+                           f"[{lo}, {hi}) ({dt:.1f} s), scaled by that chunk's share of the "
+                           f"offline full run ({t_off:.1f} s of {t_full:.0f} s over {n_chunks} "
+                           f"chunks, {thr} threads, profiles/r2/c5_oracle_chunks.jsonl)")
+    # stratified: per-root cost varies ~10x across the root id range, so each stratum of
+    # consecutive roots is timed and extrapolated by its own task share
+    import numpy as np
+
+    und = prep.export(O.X_UND_SIZE)
+    dsz = np.diff(prep.export(O.X_DIR_OFF))
+    ntask = np.where(und >= prep.p_eff - 1, dsz, 0)
+    n_str = STRATA
+    per = max(1, int(round(frac * prep.n / n_str)))
+    rng = np.random.default_rng(seed)
+    est, t_cnt, n_s, shares = t_prep, 0.0, 0, []
+    for k in range(n_str):
+        lo, hi = k * prep.n // n_str, (k + 1) * prep.n // n_str
+        roots = lo + rng.choice(hi - lo, min(per, hi - lo), replace=False)
+        tot = float(ntask[lo:hi].sum())
+        got = float(ntask[roots].sum())
+        if tot == 0 or got == 0:
+            continue
+        t1 = time.perf_counter()
+        O.count(g, p, q, workers=threads, threads=threads, capacity=cap, roots=roots,
+                prepared=prep)
+        dt = time.perf_counter() - t1
+        t_cnt += dt
+        n_s += len(roots)
+        est += dt * tot / got
+        shares.append(got / tot)
+    return None, est, (f"full CPU preprocessing ({t_prep:.1f} s) + counting {n_s} seeded roots "
+                       f"stratified over {n_str} root-id ranges ({t_cnt:.1f} s), each range "
+                       f"extrapolated by its task share")
 
 
 def load_graph(config: str, device: int | None):
