@@ -21,7 +21,11 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int64_t g_last_launches = 0;  // kernels of the last bc_graph_border call
-std::mutex g_mu;  // serialise calls (one Python thread drives the library)
+// One lock per device: calls on the same device serialise (they share its stream-ordered
+// pool and the pool reservation below); calls on different devices run concurrently, so
+// one process can drive several GPUs from several host threads (EngineConfig.devices).
+std::mutex g_dev_mu[64];
+std::mutex &dev_mu(int device) { return g_dev_mu[(unsigned)device & 63u]; }
 
 // Stream-ordered pool reservation.  Every count allocates its scratch (2-hop ids,
 // C_R1 lists, frame arenas: GBs at the FR-scale config) from the device's default
@@ -152,7 +156,7 @@ int bc_device_count(void) {
 static int graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
                         const int64_t *v_off, const int32_t *v_idx, int64_t n_v, int32_t device,
                         bool on_device, bc_graph **out) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(device));
   g_err.clear();
   *out = nullptr;
   if (n_u < 0 || n_v < 0 || !u_off || !v_off) return fail(BC_EINVAL, "invalid graph arrays");
@@ -333,7 +337,7 @@ static int count_impl(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, b
 }
 
 int bc_graph_count(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_report *out) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(h ? h->g.device : 0));
   g_err.clear();
   if (out) std::memset(out, 0, sizeof *out);
   bc::t_h2d_bytes = bc::t_d2h_bytes = 0;
@@ -348,7 +352,7 @@ int bc_graph_count(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_r
 int bc_graph_count_upper(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg,
                          const int64_t *upper_off, const int32_t *upper_ids, int64_t n_pairs,
                          bc_report *out) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(h ? h->g.device : 0));
   g_err.clear();
   if (out) std::memset(out, 0, sizeof *out);
   if (!upper_off || (n_pairs > 0 && !upper_ids) || n_pairs < 0)
@@ -366,7 +370,7 @@ int bc_graph_count_upper(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg
 int bc_assemble_upper(int32_t device, int32_t world, int64_t n, const int32_t *lens_all,
                       const int32_t *ids_all, int64_t ids_stride, int64_t *upper_off,
                       int32_t *upper_ids, int64_t ids_cap, int64_t *n_pairs) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(device));
   g_err.clear();
   try {
     if (!lens_all || !upper_off || !n_pairs || world < 1 || n < 0)
@@ -392,7 +396,7 @@ int bc_assemble_upper(int32_t device, int32_t world, int64_t n, const int32_t *l
 
 int bc_graph_twohop_slice(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, int32_t shard,
                           int32_t nshards, bc_structs **out) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(h ? h->g.device : 0));
   g_err.clear();
   try {
     if (!h || !cfg || !out) throw bc::Error(BC_EINVAL, "null argument");
@@ -429,7 +433,7 @@ int bc_count(const int64_t *u_off, const int32_t *u_idx, int64_t n_u, const int6
   if (rc != BC_OK) return rc;
   const double t1 = now_s();
   {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::mutex> lk(dev_mu(h->g.device));
     g_err.clear();
     rc = count_impl(h, p, q, cfg, out);
   }
@@ -448,7 +452,7 @@ int bc_count(const int64_t *u_off, const int32_t *u_idx, int64_t n_u, const int6
 int bc_graph_enumerate(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg,
                        int32_t *records, int64_t cap_words, int64_t *words_needed,
                        bc_report *out) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(h ? h->g.device : 0));
   g_err.clear();
   if (out) std::memset(out, 0, sizeof *out);
   try {
@@ -481,7 +485,7 @@ int bc_graph_enumerate(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg,
 
 int bc_graph_border(bc_graph *h, int32_t layer, int64_t iterations, int64_t *perm,
                     int64_t *history, int64_t *n_history) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(h ? h->g.device : 0));
   g_err.clear();
   try {
     if (!h || !history || !n_history) throw bc::Error(BC_EINVAL, "null argument");
@@ -500,7 +504,7 @@ int bc_graph_border(bc_graph *h, int32_t layer, int64_t iterations, int64_t *per
 }
 
 int bc_prepare(bc_graph *h, int32_t p, int32_t q, const bc_config *cfg, bc_structs **out) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(h ? h->g.device : 0));
   g_err.clear();
   *out = nullptr;
   bc_structs *r = new bc_structs();
@@ -568,7 +572,7 @@ static const void *export_src(const bc::DevStructs &s, int32_t what, size_t &el)
 }
 
 int bc_export_device(const bc_structs *r, int32_t what, void *device_dst) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(r ? r->g->device : 0));
   g_err.clear();
   try {
     if (!r) throw bc::Error(BC_EINVAL, "null argument");
@@ -590,7 +594,7 @@ int bc_export_device(const bc_structs *r, int32_t what, void *device_dst) {
 }
 
 int bc_export(const bc_structs *r, int32_t what, void *dst) {
-  std::lock_guard<std::mutex> lk(g_mu);
+  std::lock_guard<std::mutex> lk(dev_mu(r ? r->g->device : 0));
   g_err.clear();
   try {
     if (!r || !dst) throw bc::Error(BC_EINVAL, "null argument");

@@ -12,7 +12,10 @@ Mirrors the reference engine surface (``pkg/src/bicount/engine.py``):
   (engine.py:115-144) — built on the GPU, exported back to host arrays.
 
 ``worker_count`` is validated exactly as in the reference but does not
-change the device schedule (warps pull tasks from one atomic queue).
+change the device schedule (warps pull tasks from one atomic queue).  The
+reference's in-call parallelism (engine.py:449-478: one call, several workers)
+maps to ``EngineConfig(devices=(0, 1, ...))``: one host thread per listed GPU,
+each counting its shard of the tasks, exact partials summed in the call.
 """
 
 from __future__ import annotations
@@ -50,6 +53,7 @@ class EngineConfig:
     restricted_rows: bool = True  # scatter walks read N(v) & dir2(root), not all of N(v)
     force_triage: bool = False    # p_eff >= 5: filter + triage path whatever the task count
     shard_mode: str = "root"  # multi-GPU: whole roots, degree-balanced | "task" interleave
+    devices: tuple | None = None  # one call over several GPUs (thread per device); None: device
 
     def validate(self) -> None:
         if self.worker_count < 1:
@@ -66,6 +70,9 @@ class EngineConfig:
             raise ValueError(f"level1 / rows must be one of {KERNEL_CHOICES}")
         if self.shard_mode not in ("root", "task"):
             raise ValueError("shard_mode must be one of ('root', 'task')")
+        if self.devices is not None and (len(self.devices) < 1 or
+                                         any(int(d) < 0 for d in self.devices)):
+            raise ValueError("devices must list at least one device index >= 0")
 
 
 @dataclass
@@ -444,18 +451,85 @@ def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
         claims = np.zeros(cap, dtype=np.uint32)
         c.task_claims = claims.ctypes.data
         c.task_claims_cap = cap
-    rep = _abi.BcReport()
-    _abi.check(L.bc_count(uo.ctypes.data, ui.ctypes.data, nu, vo.ctypes.data, vi.ctypes.data, nv,
-                          int(pp), int(qq), C.byref(c), C.byref(rep)))
+    devs = tuple(int(d) for d in cfg.devices) if cfg.devices else (int(cfg.device),)
+    if len(devs) == 1:
+        c.device = devs[0]
+        rep = _abi.BcReport()
+        _abi.check(L.bc_count(uo.ctypes.data, ui.ctypes.data, nu, vo.ctypes.data, vi.ctypes.data,
+                              nv, int(pp), int(qq), C.byref(c), C.byref(rep)))
+        wall = rep.time_level1 + rep.time_enum
+    else:
+        rep, wall = _count_devices(L, (uo, ui, vo, vi), nu, nv, pp, qq, c, devs, claims)
     del keep
     layer = structures.choice.layer if structures is not None else "UV"[rep.anchor]
-    out = _report(rep, cfg, rep.time_level1 + rep.time_enum, layer)
+    out = _report(rep, cfg, wall, layer)
     if claims is not None:
         out.task_tally, out.task_counts = task_tally(claims, rep.tasks_emitted, cfg.worker_count)
     if cfg.enumerate_results:
         out.bicliques = enumerate_bicliques(graph, pp, qq, cfg, out.count, layer, anchor=anchor,
                                             rank=rank, roots=roots)
     return out
+
+
+# report fields summed over the shards of one multi-device call (the rest are global:
+# equal on every shard) and the phase times taken as the slowest shard's
+_SUMMED = ("tasks_consumed", "tasks_stolen", "batches_executed", "tasks_alive", "tasks_split",
+           "intersections", "operand_words", "min_words", "kernel_launches", "h2d_bytes",
+           "d2h_bytes", "level1_operand_words", "nesting_checked", "level1_entries")
+_MAXED = ("time_h2d", "time_prep", "time_level1", "time_enum", "time_total")
+
+
+def _count_devices(L, csr, nu, nv, p, q, c, devs, claims):
+    """One call over several GPUs (the reference's in-call workers, engine.py:449-478):
+    shard k of len(devs) on devs[k], one host thread each (ctypes drops the GIL; the
+    library locks per device), exact u128 partials summed.  Returns (merged report,
+    wall time of the counting phase = the slowest shard's level 1 + enumeration)."""
+    import threading
+
+    uo, ui, vo, vi = csr
+    n = len(devs)
+    reps = [_abi.BcReport() for _ in range(n)]
+    cfgs, logs, errs = [], [], [None] * n
+    for k, d in enumerate(devs):
+        ck = _abi.BcConfig()
+        C.pointer(ck)[0] = c  # copy every field, then this shard's device and index
+        ck.device, ck.shard_index, ck.shard_count = d, k, n
+        if claims is not None:
+            lg = np.zeros_like(claims)
+            ck.task_claims, ck.task_claims_cap = lg.ctypes.data, len(lg)
+            logs.append(lg)
+        cfgs.append(ck)
+
+    def run(k):
+        try:
+            _abi.check(L.bc_count(uo.ctypes.data, ui.ctypes.data, nu, vo.ctypes.data,
+                                  vi.ctypes.data, nv, int(p), int(q), C.byref(cfgs[k]),
+                                  C.byref(reps[k])))
+        except Exception as e:  # re-raised on the calling thread
+            errs[k] = e
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    out = _abi.BcReport()
+    C.pointer(out)[0] = reps[0]
+    total = sum(int(r.count_lo) | (int(r.count_hi) << 64) for r in reps)
+    if total >> 128:
+        raise RuntimeError("bicount_b200 error: the count reached 2^128")
+    out.count_lo, out.count_hi = total & ((1 << 64) - 1), total >> 64
+    out.overflow = max(r.overflow for r in reps)
+    for f in _SUMMED:
+        setattr(out, f, sum(getattr(r, f) for r in reps))
+    for f in _MAXED:
+        setattr(out, f, max(getattr(r, f) for r in reps))
+    if claims is not None:
+        claims[:] = np.sum(logs, axis=0)
+    return out, max(r.time_level1 + r.time_enum for r in reps)
 
 
 ENUM_GUARD = 10**7

@@ -123,3 +123,23 @@ def test_enumeration_with_roots_and_structures(anchor):
     r = count_bicliques(g, p, q, EngineConfig(enumerate_results=True, anchor=anchor),
                         roots=range(0, 5))
     assert r.count == len(r.bicliques) and set(r.bicliques) <= set(want)
+
+
+@pytest.mark.parametrize("devs", [(0, 0), (0, 0, 0)])
+def test_one_call_over_several_devices(golden, devs):
+    """The reference's in-call parallelism (engine.py:449-478: one count_bicliques call,
+    several workers) as EngineConfig(devices=...): a host thread per listed GPU counts its
+    shard and the call sums the exact partials.  Only one GPU is reachable here, so the
+    shards share device 0 (the library serialises calls per device); the merge, the
+    counters and the claim log are what is checked."""
+    for name, (p, q) in (("C4", (8, 8)), ("C3", (6, 3)), ("C1", (2, 2))):
+        g = synth.build_config(name)
+        want = golden["configs"][name][f"({p},{q})"]["hybrid"]
+        rep = count_bicliques(g, p, q, EngineConfig(devices=devs, track_tasks=True))
+        assert str(rep.count) == want["count"], name
+        assert rep.batches_executed == want["batches"], name
+        assert rep.tasks_emitted == want["emitted"]
+        assert rep.tasks_consumed == want["emitted"]  # every task by exactly one shard
+        assert sorted(rep.task_tally) == [(0, i) for i in range(want["emitted"])]
+    with pytest.raises(ValueError):
+        EngineConfig(devices=()).validate()
