@@ -17,6 +17,32 @@ namespace bc {
 thread_local int64_t t_h2d_bytes = 0, t_d2h_bytes = 0;
 }
 
+namespace bc {
+
+cudaMemPool_t lib_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[device] = p;
+  }
+  return pools[device];
+}
+
+}  // namespace bc
+
 namespace {
 
 thread_local std::string g_err;
@@ -42,12 +68,12 @@ void pool_reserve(int device, int64_t n_edges, cudaStream_t st) {
   const size_t base = (size_t)n_edges * 160 + (size_t(256) << 20), high = g_pool_high[device];
   if (g_pool_reserved[device] >= std::max(base, high + high / 10)) return;
   const size_t want = std::max(base, high + high / 2);
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  cudaMemPool_t pool = bc::lib_pool(device);
+  if (!pool) return;
   cudaStreamSynchronize(st);
   cudaMemPoolTrimTo(pool, 0);
   void *p = nullptr;
-  if (cudaMallocAsync(&p, want, st) == cudaSuccess) {
+  if (cudaMallocFromPoolAsync(&p, want, pool, st) == cudaSuccess) {
     cudaFreeAsync(p, st);
     cudaStreamSynchronize(st);
     g_pool_reserved[device] = want;
@@ -59,8 +85,8 @@ void pool_reserve(int device, int64_t n_edges, cudaStream_t st) {
 
 void pool_record(int device) {
   if (device < 0 || device >= 64) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  cudaMemPool_t pool = bc::lib_pool(device);
+  if (!pool) return;
   unsigned long long high = 0;
   if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high) == cudaSuccess &&
       (size_t)high > g_pool_high[device])
@@ -180,24 +206,16 @@ static int graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
     bc::DevGraph &g = h->g;
     g.device = device;
     BC_CUDA(cudaSetDevice(device));
-    {
-      // keep freed stream-ordered allocations cached in the pool: the default
-      // release threshold (0) hands memory back at every synchronisation and
-      // turns the next call's scratch allocations into driver remaps
-      cudaMemPool_t pool;
-      BC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-      uint64_t keep = UINT64_MAX;
-      BC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    }
+    if (!bc::lib_pool(device)) throw bc::Error(BC_ECUDA, "cannot create the device memory pool");
     BC_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
     g.n_u = n_u;
     g.n_v = n_v;
     g.n_e = e;
     cudaStream_t st = g.stream;
-    BC_CUDA(cudaMallocAsync((void **)&g.u_off, (n_u + 1) * 8, st));
-    BC_CUDA(cudaMallocAsync((void **)&g.v_off, (n_v + 1) * 8, st));
-    BC_CUDA(cudaMallocAsync((void **)&g.u_idx, (e ? e : 1) * 4, st));
-    BC_CUDA(cudaMallocAsync((void **)&g.v_idx, (e ? e : 1) * 4, st));
+    BC_CUDA(bc::pool_malloc((void **)&g.u_off, (n_u + 1) * 8, st));
+    BC_CUDA(bc::pool_malloc((void **)&g.v_off, (n_v + 1) * 8, st));
+    BC_CUDA(bc::pool_malloc((void **)&g.u_idx, (e ? e : 1) * 4, st));
+    BC_CUDA(bc::pool_malloc((void **)&g.v_idx, (e ? e : 1) * 4, st));
     if (on_device) {  // device-resident input (e.g. a torch CUDA tensor): D2D copy
       BC_CUDA(cudaMemcpyAsync(g.u_off, u_off, (n_u + 1) * 8, cudaMemcpyDeviceToDevice, st));
       BC_CUDA(cudaMemcpyAsync(g.v_off, v_off, (n_v + 1) * 8, cudaMemcpyDeviceToDevice, st));
@@ -216,8 +234,8 @@ static int graph_create(const int64_t *u_off, const int32_t *u_idx, int64_t n_u,
     // wedge mass + max degree per layer (graph.py:246-249), once per graph
     unsigned long long *dw;
     int *dm;
-    BC_CUDA(cudaMallocAsync((void **)&dw, 16, st));
-    BC_CUDA(cudaMallocAsync((void **)&dm, 8, st));
+    BC_CUDA(bc::pool_malloc((void **)&dw, 16, st));
+    BC_CUDA(bc::pool_malloc((void **)&dm, 8, st));
     BC_CUDA(cudaMemsetAsync(dw, 0, 16, st));
     BC_CUDA(cudaMemsetAsync(dm, 0, 8, st));
     const int sms = bc::num_sms(device);

@@ -22,6 +22,17 @@ struct DevGraph {
   int64_t wedge_u = 0, wedge_v = 0;  // sum C(d,2) per layer (graph.py:246-249)
 };
 
+// The library's own stream-ordered pool on each device (created on first use, release
+// threshold UINT64_MAX so freed scratch stays cached between calls).  Private, so the
+// caching never changes the device's default pool that PyTorch or NCCL allocate from.
+cudaMemPool_t lib_pool(int device);
+inline cudaError_t pool_malloc(void **p, size_t bytes, cudaStream_t st) {
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes, lib_pool(d), st);
+}
+
 // Stream-ordered device buffer.
 template <typename T>
 struct DBuf {
@@ -44,7 +55,7 @@ struct DBuf {
     release();
     s = stream;
     n = count;
-    BC_CUDA(cudaMallocAsync((void **)&p, (count ? count : 1) * sizeof(T), stream));
+    BC_CUDA(pool_malloc((void **)&p, (count ? count : 1) * sizeof(T), stream));
   }
   void zero() { if (n) BC_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
   void release() {

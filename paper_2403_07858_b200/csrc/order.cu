@@ -140,12 +140,12 @@ void build_view(const int64_t *off, const int32_t *idx, int64_t n, const int32_t
   row_counts<<<wb, 256, 0, st>>>(off, idx, n, newa, newb, cnt.p);
   BC_CHECK_LAUNCH();
   int64_t *noff;
-  BC_CUDA(cudaMallocAsync((void **)&noff, (na + 1) * 8, st));
+  BC_CUDA(pool_malloc((void **)&noff, (na + 1) * 8, st));
   scan_excl(cnt.p, noff, na + 1, st);
   BC_CUDA(cudaMemcpyAsync(&ne, noff + na, 8, cudaMemcpyDeviceToHost, st));
   BC_CUDA(cudaStreamSynchronize(st));
   int32_t *nidx;
-  BC_CUDA(cudaMallocAsync((void **)&nidx, (ne ? ne : 1) * 4, st));
+  BC_CUDA(pool_malloc((void **)&nidx, (ne ? ne : 1) * 4, st));
   row_write<<<wb, 256, 0, st>>>(off, idx, n, newa, newb, noff, nidx);
   BC_CHECK_LAUNCH();
   L += 3;
