@@ -22,6 +22,8 @@ from .engine import (
     merge_limbs,
     prepare_structures,
     split_limbs,
+    stats_payload,
+    write_stats_json,
 )
 from .graph import BipartiteGraph, CsrView, as_csr, from_edges, transpose
 
@@ -31,5 +33,6 @@ __all__ = [
     "AnchorChoice", "BipartiteGraph", "CountReport", "CsrView", "DeviceGraph", "EngineConfig",
     "Htb", "PriorityOrder", "SearchStructures", "TwoHopIndex", "allreduce_count", "as_csr",
     "count_bicliques", "count_bicliques_distributed", "from_edges", "merge_limbs",
-    "prepare_structures", "split_limbs", "transpose", "__version__",
+    "prepare_structures", "split_limbs", "stats_payload", "transpose", "write_stats_json",
+    "__version__",
 ]

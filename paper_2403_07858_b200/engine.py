@@ -254,6 +254,35 @@ class DeviceGraph:
         del keep
         return out[0], out[1]
 
+    def htb_arenas(self, p: int, q: int, cfg: EngineConfig | None = None, *, anchor=None,
+                   rank=None):
+        """The device-built HTB arenas of (p, q) as CUDA tensors, without a host round trip:
+        {"adj": (off int64, idx int32, val int32), "dir2": (...)} -- the u32 words of
+        htb.py:64-86 viewed as int32 (compare with ``htb.load_htb_device``)."""
+        import torch
+
+        cfg = cfg if cfg is not None else EngineConfig()
+        cfg.validate()
+        L = _abi.load()
+        c, keep = _make_config(cfg, anchor or cfg.anchor, rank, None)
+        h = C.c_void_p()
+        _abi.check(L.bc_prepare(self._h, int(p), int(q), C.byref(c), C.byref(h)))
+        try:
+            dev = torch.device("cuda", cfg.device)
+            out = {}
+            for name, ids in (("adj", (_abi.BC_X_HADJ_OFF, _abi.BC_X_HADJ_IDX, _abi.BC_X_HADJ_VAL)),
+                              ("dir2", (_abi.BC_X_HDIR_OFF, _abi.BC_X_HDIR_IDX, _abi.BC_X_HDIR_VAL))):
+                ts = []
+                for what, dt in zip(ids, (torch.int64, torch.int32, torch.int32)):
+                    t = torch.empty(max(int(L.bc_export_len(h, what)), 0), dtype=dt, device=dev)
+                    _abi.check(L.bc_export_device(h, what, t.data_ptr() if t.numel() else None))
+                    ts.append(t)
+                out[name] = tuple(ts)
+        finally:
+            L.bc_structs_destroy(h)
+        del keep
+        return out
+
     def count_raw(self, p: int, q: int, cfg: EngineConfig | None = None, *, anchor=None,
                   rank=None, roots=None, shard=(0, 1), task_counts: bool = False, upper=None):
         """One counting pass; returns (BcReport, per-task counts or None).  ``upper`` =
@@ -469,6 +498,34 @@ def count_bicliques(g, p: int, q: int, cfg: EngineConfig | None = None, *,
         out.bicliques = enumerate_bicliques(graph, pp, qq, cfg, out.count, layer, anchor=anchor,
                                             rank=rank, roots=roots)
     return out
+
+
+# CountReport fields of the reference (engine.py:64-79); cli.py:252-257 writes them as
+# {"schema": 1, **asdict(report)} for --stats-json
+REFERENCE_REPORT_FIELDS = ("count", "time_1hop", "time_2hop", "batches_executed", "tasks_stolen",
+                           "roots_filtered", "wall_time", "tasks_emitted", "tasks_consumed",
+                           "workers", "anchor_layer", "bicliques", "task_tally", "task_counts")
+
+
+def stats_payload(report: CountReport, include_device: bool = False) -> dict:
+    """The reference CLI's --stats-json payload for this report (cli.py:252-257): schema 1
+    plus the reference's CountReport fields, in its order; ``device`` (this library's own
+    measurements) only when asked for."""
+    d = {"schema": 1}
+    for k in REFERENCE_REPORT_FIELDS:
+        d[k] = getattr(report, k)
+    if include_device:
+        d["device"] = dict(report.device)
+    return d
+
+
+def write_stats_json(report: CountReport, path, include_device: bool = False) -> None:
+    """cli.py:252-257: json.dump(payload, indent=2, default=int) and a newline."""
+    import json
+
+    with open(path, "w") as fh:
+        json.dump(stats_payload(report, include_device), fh, indent=2, default=int)
+        fh.write("\n")
 
 
 # report fields summed over the shards of one multi-device call (the rest are global:

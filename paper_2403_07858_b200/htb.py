@@ -152,3 +152,16 @@ def load_htb(path) -> Htb:
     if len(off) != n_sets + 1 or len(idx) != n_words or len(val) != n_words:
         raise ValueError(f"{path}: truncated dump")
     return Htb(off.astype(np.int64), idx.astype(np.uint32), val.astype(np.uint32))
+
+
+def load_htb_device(path, device: int = 0):
+    """A dump straight into device memory (CUDA tensors off int64, idx int32, val int32 --
+    the u32 words viewed as int32, the layout of ``DeviceGraph.htb_arenas``): the file is
+    read once into pinned host memory and copied with one transfer per array."""
+    import torch
+
+    h = load_htb(path)
+    dev = torch.device("cuda", device)
+    return tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+                 for a in (h.off.astype(np.int64), h.idx.view(np.int32), h.val.view(np.int32)))
+

@@ -112,3 +112,47 @@ def test_slices_and_intersections():
         assert r.decode() == sorted(set(xs) & set(ys))
         assert htb.htb_intersect_count(sa, sb) == len(set(xs) & set(ys)) == r.cardinality()
         assert sa.cardinality() == len(xs)
+
+
+def test_stats_json_payload_matches_reference_schema(tmp_path):
+    """cli.py:252-257: {"schema": 1, **asdict(report)} over the reference's CountReport
+    fields (engine.py:64-79), json with default=int and a trailing newline."""
+    import json
+
+    from paper_2403_07858_b200 import CountReport, stats_payload, write_stats_json
+
+    r = CountReport(count=1 << 70, time_1hop=0.5, time_2hop=1.5, batches_executed=7,
+                    tasks_stolen=0, roots_filtered=2, wall_time=2.0, tasks_emitted=9,
+                    tasks_consumed=9, workers=1, anchor_layer="U", device={"kernel_launches": 3})
+    d = stats_payload(r)
+    assert list(d) == ["schema", "count", "time_1hop", "time_2hop", "batches_executed",
+                       "tasks_stolen", "roots_filtered", "wall_time", "tasks_emitted",
+                       "tasks_consumed", "workers", "anchor_layer", "bicliques", "task_tally",
+                       "task_counts"]
+    p = tmp_path / "s.json"
+    write_stats_json(r, p)
+    raw = p.read_text()
+    assert raw.endswith("}\n") and json.loads(raw)["count"] == 1 << 70
+    assert "device" in stats_payload(r, include_device=True)
+
+
+@pytest.mark.gpu
+def test_dump_loads_straight_into_device_arenas(tmp_path):
+    """A HTBDUMP1 dump of the device-built arenas, loaded back straight into device memory
+    (htb.load_htb_device), equals the arenas word for word."""
+    import torch
+
+    from paper_2403_07858_b200 import DeviceGraph, prepare_structures
+
+    g = synth.build_config("C4")
+    s = prepare_structures(g, 8, 8)
+    dg = DeviceGraph(g)
+    try:
+        arenas = dg.htb_arenas(8, 8)
+    finally:
+        dg.close()
+    for name, h in (("adj", s.adj_htb), ("dir2", s.dir2_htb)):
+        htb.dump_htb(h, tmp_path / f"{name}.bin")
+        got = htb.load_htb_device(tmp_path / f"{name}.bin", 0)
+        for a, b in zip(got, arenas[name]):
+            assert a.dtype == b.dtype and torch.equal(a, b), name
