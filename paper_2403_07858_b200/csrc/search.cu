@@ -834,6 +834,7 @@ struct DbgTimer {
 // the others go to the medium list as before.
 // ---------------------------------------------------------------------------
 constexpr int RF_THREADS = 256;
+constexpr int RF_RUN = 32;  // tasks claimed per warp at a time
 
 __global__ void __launch_bounds__(RF_THREADS, 4) rfilter_kernel(Params P, EnumArgs A,
                                                                int budget_words) {
@@ -844,19 +845,43 @@ __global__ void __launch_bounds__(RF_THREADS, 4) rfilter_kernel(Params P, EnumAr
   Acc128 total{0, 0, 0};
   unsigned long long claims = 0;
   const int q = P.q_eff;
+  // tasks are claimed RF_RUN at a time and lane k resolves task k's chain of dependent
+  // loads (queue -> task -> root offsets -> rank position, list offset, level-1 facts)
+  // for the whole run at once; the warp then takes the run's tasks one by one
+  int nb = 0, k = 0;
+  int b_j = 0, b_rps = 0;
+  int64_t b_t = 0, b_l0 = 0;
+  int b_nR = 0, b_nL = 0, b_wR = 0, b_wL = 0;
   BC_LOOP
   for (;;) {
-    long long qi = 0;
-    if (lane == 0) qi = (long long)atomicAdd(P.ctr + CTR_NEXT, 1ull);
-    qi = __shfl_sync(FULL, qi, 0) + A.q0;
-    if (qi >= A.q1) break;
+    if (k >= nb) {
+      long long q0 = 0;
+      if (lane == 0) q0 = (long long)atomicAdd(P.ctr + CTR_NEXT, (unsigned long long)RF_RUN);
+      q0 = __shfl_sync(FULL, q0, 0) + A.q0;
+      if (q0 >= A.q1) break;
+      nb = (int)min((long long)RF_RUN, A.q1 - q0);
+      k = 0;
+      if (lane < nb) {
+        b_j = A.queue[q0 + lane];
+        b_t = task_id(P.ltask, P.shard, P.nshards, b_j);
+        const int br = P.tasks[b_t].x;
+        b_rps = P.rpos[P.dir_off[br] + (b_t - P.troot[br])];
+        b_l0 = P.roff[b_j];
+        const Info in = A.info[b_j];
+        b_nR = in.cr;
+        b_nL = in.cl;
+        b_wR = in.wr;
+        b_wL = in.wl;
+      }
+    }
     claims++;
-    const int j = A.queue[qi];
-    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
-    const int r = P.tasks[t].x;
-    const int64_t d0 = P.dir_off[r];
-    const int rps = P.rpos[d0 + (t - P.troot[r])];  // candidates: positions [0, rps)
-    const Dims d = dims_of(A.info[j]);
+    const int j = __shfl_sync(FULL, b_j, k);
+    const int64_t t = __shfl_sync(FULL, b_t, k);
+    const int rps = __shfl_sync(FULL, b_rps, k);  // candidates: positions [0, rps)
+    const int64_t lbase = __shfl_sync(FULL, b_l0, k);
+    const Dims d = dims_of(Info{__shfl_sync(FULL, b_nR, k), __shfl_sync(FULL, b_wR, k),
+                                __shfl_sync(FULL, b_nL, k), __shfl_sync(FULL, b_wL, k)});
+    k++;
     bool surv = false;
     if (rps > 2 * budget_words) {
       surv = true;  // counters do not fit: the triage kernel decides
@@ -864,7 +889,6 @@ __global__ void __launch_bounds__(RF_THREADS, 4) rfilter_kernel(Params P, EnumAr
       BC_LOOP
       for (int w = lane; w < (rps + 1) / 2; w += 32) cnt[w] = 0;
       __syncwarp();
-      const int64_t lbase = P.roff[j];
       BC_LOOP
       for (int b0 = 0; b0 < d.nR && !surv; b0 += 32) {
         const int i = b0 + lane;
