@@ -96,7 +96,7 @@ __global__ void p1_kernel(Params P, const int64_t *__restrict__ deg_off) {
 // ---------------------------------------------------------------------------
 // level 1 (engine.py:265-299 up to the descent)
 // ---------------------------------------------------------------------------
-template <bool INSTR>
+template <bool INSTR, int RUN>
 __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict__ info,
                                                      uint32_t *__restrict__ cost) {
   const int lane = lane_id();
@@ -105,32 +105,48 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
   const int64_t nloc = P.n_local;
   Acc128 a{0, 0};
   unsigned long long alive = 0, inter = 0, opw = 0, minw = 0, maxro = 0, maxscr = 0, claimed = 0;
-  for (int64_t j = gw; j < nloc; j += nw) {
-    const int64_t t = task_id(P.ltask, P.shard, P.nshards, j);
-    const int2 tk = P.tasks[t];
+  // runs of 32 consecutive local tasks per warp: lane k resolves task k's loads (task,
+  // list offsets, member-id base) for the run at once, then the warp takes them in turn
+  int64_t b_t = 0, b_l0 = 0, b_l1 = 0, b_ab = 0;
+  int2 b_tk{0, 0};
+  // (RUN = 32 only when there are many tasks per warp: C5's 18.9 M, not C2's 0.7 M)
+  for (int64_t j0 = gw * RUN; j0 < nloc; j0 += nw * RUN) {
+    const int nrun = (int)min((int64_t)RUN, nloc - j0);
+    if (RUN == 1 || lane < nrun) {
+      const int64_t jl = RUN == 1 ? j0 : j0 + lane;  // RUN = 1: every lane loads task j0
+      b_t = task_id(P.ltask, P.shard, P.nshards, jl);
+      b_tk = P.tasks[b_t];
+      if (P.lists) {
+        b_l0 = P.roff[jl];
+        b_l1 = P.roff[jl + 1];
+        if (P.roffE) b_ab = P.csr_aoff[b_tk.x] - P.rebase[b_tk.x];
+      }
+    }
+  for (int kk = 0; kk < nrun; kk++) {
+    const int64_t j = j0 + kk;
+    const int64_t t = RUN == 1 ? b_t : __shfl_sync(FULL, b_t, kk);
+    const int2 tk = RUN == 1 ? b_tk : int2{__shfl_sync(FULL, b_tk.x, kk), __shfl_sync(FULL, b_tk.y, kk)};
     claimed++;
     if (P.claims && lane == 0) atomicAdd(P.claims + t, 1u);
     int cr, wr;
     if (P.lists) {  // C_R1 from the wedge-scatter pass: |C_R1| and its HTB word count
-      const int64_t l0 = P.roff[j];
-      cr = (int)(P.roff[j + 1] - l0);
+      const int64_t l0 = RUN == 1 ? b_l0 : __shfl_sync(FULL, b_l0, kk);
+      cr = (int)((RUN == 1 ? b_l1 : __shfl_sync(FULL, b_l1, kk)) - l0);
+      const int64_t ab = RUN == 1 ? b_ab : __shfl_sync(FULL, b_ab, kk);
       wr = 0;
+      uint32_t last = 0xffffffffu;  // word of the previous batch's last member
       for (int b = 0; b < cr; b += 32) {
         const int i = b + lane;
-        bool start = false;
+        uint32_t w = 0xffffffffu;
         if (i < cr) {
-          uint32_t w, wp = 0;
-          if (P.roffE) {  // edge-indexed list: member ids through the anchor CSR
-            const int64_t ab = P.csr_aoff[tk.x] - P.rebase[tk.x];
-            w = (uint32_t)__ldg(P.csr_aidx + ab + __ldg(P.lists + l0 + i)) >> 5;
-            if (i > 0) wp = (uint32_t)__ldg(P.csr_aidx + ab + __ldg(P.lists + l0 + i - 1)) >> 5;
-          } else {
-            w = (uint32_t)__ldg(P.lists + l0 + i) >> 5;
-            if (i > 0) wp = (uint32_t)__ldg(P.lists + l0 + i - 1) >> 5;
-          }
-          start = i == 0 || wp != w;
+          // edge-indexed list: member ids through the anchor CSR
+          w = P.roffE ? (uint32_t)__ldg(P.csr_aidx + ab + __ldg(P.lists + l0 + i)) >> 5
+                      : (uint32_t)__ldg(P.lists + l0 + i) >> 5;
         }
-        wr += __popc(__ballot_sync(FULL, start));
+        uint32_t wp = __shfl_up_sync(FULL, w, 1);
+        if (lane == 0) wp = last;
+        wr += __popc(__ballot_sync(FULL, i < cr && (i == 0 || wp != w)));
+        last = __shfl_sync(FULL, w, 31);
       }
     } else {
       wr = isect_adj<false>(P.g, tk.x, tk.y, cr, nullptr, nullptr, nullptr);
@@ -179,6 +195,7 @@ __global__ void __launch_bounds__(256) level1_kernel(Params P, Info *__restrict_
       }
     }
     a.add(one);  // lane-uniform: only lane 0 contributes below
+  }
   }
   if (lane == 0) {
     atomic_add128(P.acc, P.overflow, a);
@@ -1340,8 +1357,11 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
     {
       int64_t blocks = (nloc * 32 + 255) / 256;
       blocks = std::min<int64_t>(blocks, (int64_t)sms * 32);
-      if (instr) level1_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
-      else level1_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
+      const bool runs = nloc >= blocks * 8 * 128;  // many tasks per warp: batched loads
+      if (instr && runs) level1_kernel<true, 32><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
+      else if (instr) level1_kernel<true, 1><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
+      else if (runs) level1_kernel<false, 32><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
+      else level1_kernel<false, 1><<<(unsigned)blocks, 256, 0, st>>>(P, info.p, cost.p);
       BC_CHECK_LAUNCH();
       dt.mark("level1_kernel");
       launches++;
