@@ -1627,7 +1627,10 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           // split mode (p_eff >= 5): chunks of the LPT queue; per chunk, enum_kernel
             // writes every frame to the frame arena and pushes the split-level nodes,
             // then sub_kernel drains them heaviest first with every warp.
-            const int split_level = s.p_eff <= 6 ? 2 : 3;
+            // sub-tasks at level 2, or at level 3 when p_eff > 6 and there are too few heavy
+            // tasks to fill the GPU at level 2 (C4: three planted cores, 2.8 vs 6.4 ms;
+            // C5H: 2.9e5 heavy tasks, level 2 is 7% faster than 3)
+            const int split_level = s.p_eff <= 6 || n_heavy >= 65536 ? 2 : 3;
             const int budget = 1024;
             const size_t smem = (size_t)wpb * (budget + map_w + LEAF_WORDS) * 4;
             const EnumVariant ev{instr, false, true, false};
