@@ -275,6 +275,9 @@ struct Frame {
   int o_cand, o_setR, o_setL, o_surv, o_ns, o_cur;
   int surv_cap;
   bool compact;
+  // every node of this task fits one reference batch (|C_L1| * max(words) <= capacity, or
+  // dfs mode): node_batches then needs no HTB word counts, so they are not computed
+  bool skip_words;
   __device__ __forceinline__ uint32_t *r_idx() const { return (uint32_t *)(ro + o_r_idx); }
   __device__ __forceinline__ uint32_t *r_val() const { return (uint32_t *)(ro + o_r_val); }
   __device__ __forceinline__ int *r_pre() const { return (int *)(ro + o_r_pre); }
@@ -367,6 +370,15 @@ __device__ __forceinline__ void carve_ro(Frame &f, uint32_t *p, const Dims &d,
   f.o_adjw = o; if (sp.instr) o += d.nL;
   f.o_dirw = o;
   f.compact = sp.compact;
+  f.skip_words = false;
+}
+
+// set once per task (frame or sub-task) in non-instrumented launches: a node's candidates
+// are a subset of C_L1 and its word counts at most C_R1's / C_L1's, so node_batches is
+// (ncand > 0) whenever |C_L1| * max(words(C_R1), words(C_L1), 1) fits the capacity
+__device__ __forceinline__ void set_skip_words(Frame &f, const Params &P, const Dims &d, bool instr) {
+  const int64_t wm = d.wR > d.wL ? (d.wR > 1 ? d.wR : 1) : (d.wL > 1 ? d.wL : 1);
+  f.skip_words = !instr && (P.mode_dfs || (int64_t)d.nL * wm <= (int64_t)P.cap);
 }
 
 __device__ __forceinline__ void carve_scratch(Frame &f, uint32_t *p, const Dims &d, int p_eff,
@@ -747,7 +759,7 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
     const int u = act ? list[i] : 0;
     const uint32_t *ru_mine = act ? rowR_of(f, d, u) : nullptr;
     const uint32_t *ru2 = act && list2 ? rowR_of(f, d, list2[i]) : nullptr;
-    const int wr = act ? lane_words(R, ru_mine, f.r_last(), WR, ru2) : 0;
+    const int wr = act ? (f.skip_words ? 1 : lane_words(R, ru_mine, f.r_last(), WR, ru2)) : 0;
     uint32_t rp[RP_WORDS];
 #pragma unroll
     for (int x = 0; x < RP_WORDS; x++)
@@ -851,8 +863,8 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
     uint32_t rp[RP_WORDS];
 #pragma unroll
     for (int x = 0; x < RP_WORDS; x++) rp[x] = act && x < WR ? R[x] & ru[x] : 0u;
-    const int wr_u = act ? lane_words(R, ru, f.r_last(), WR) : 0;
-    const int wl_u = act ? lane_words(Ls, rl, f.l_last(), WL) : 0;
+    const int wr_u = act ? (f.skip_words ? 1 : lane_words(R, ru, f.r_last(), WR)) : 0;
+    const int wl_u = act ? (f.skip_words ? 1 : lane_words(Ls, rl, f.l_last(), WL)) : 0;
     int ncand_u = 0;
     BC_LOOP
     for (int x = 0; __any_sync(FULL, act && x < WL); x++) {
@@ -977,8 +989,8 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
     ncand = __reduce_add_sync(FULL, c);
     ncand_eval = compact_bits_and(Ls, f.s1(), WL, f.cand());
   }
-  const int wr = level == 1 ? d.wR : words_touched(R, f.r_last(), WR);
-  const int wl = leaf ? 0 : (level == 1 ? d.wL : words_touched(Ls, f.l_last(), WL));
+  const int wr = level == 1 ? d.wR : f.skip_words ? 1 : words_touched(R, f.r_last(), WR);
+  const int wl = leaf ? 0 : (level == 1 ? d.wL : f.skip_words ? 1 : words_touched(Ls, f.l_last(), WL));
   if (lane == 0) tl.batches += node_batches(P, (unsigned)ncand, wr, wl, leaf);
   int ns = 0;
   const int need_l = P.p_eff - level - 2;  // prune_keep(cr, cl, level+1): cl >= p - (level+1) - 1
@@ -1638,6 +1650,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) enum_kernel(Par
     Frame f;
     carve_ro(f, ro_base, d, sp);
     carve_scratch(f, sc_base, d, p_eff, sp);
+    set_skip_words(f, P, d, INSTR);
     const int ns1 = build_frame_R<INSTR>(P, f, d, sp, tk.x, tk.y, j, map, ph_);
     if (TRIAGE && ns1 > A.triage) {  // too many survivor rows: split path
       if (lane == 0) push_heavy(P, A, j, ns1);
@@ -1724,6 +1737,7 @@ __global__ void __launch_bounds__(ENUM_THREADS, ENUM_MIN_BLOCKS) sub_kernel(Para
     Frame f;
     carve_ro(f, A.frames + foff, d, sp);
     carve_scratch(f, sc_base, d, p_eff, sp);
+    set_skip_words(f, P, d, INSTR);
     BC_LOOP
     for (int w = lane; w < d.WR; w += 32) f.setR()[(lv - 1) * d.WR + w] = rec[4 + w];
     BC_LOOP
