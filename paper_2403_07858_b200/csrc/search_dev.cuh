@@ -921,9 +921,9 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
               tl.minw += wlo < f.dirw()[w] ? wlo : f.dirw()[w];
             }
             const uint32_t *rlo = rowL_of(f, d, uo), *rlw = rowL_of(f, d, w);
-            int cl = 0;
+            int cl = 0;  // only |L'| >= need_g matters: stop once it is reached
             BC_LOOP
-            for (int x2 = 0; x2 < WL; x2++) cl += __popc(Ls[x2] & rlo[x2] & rlw[x2]);
+            for (int x2 = 0; x2 < WL && cl < need_g; x2++) cl += __popc(Ls[x2] & rlo[x2] & rlw[x2]);
             keep = cl >= need_g;
           }
         }
@@ -1025,9 +1025,9 @@ __device__ __forceinline__ int expand(const Params &P, const Frame &f, const Dim
             keep = true;  // |L'| >= 1 is checked when the leaf-parent is walked
           } else {
             const uint32_t *rl = rowL_of(f, d, u);
-            int cl = 0;
+            int cl = 0;  // prune_keep only needs |L'| >= need_l: stop once it is reached
             BC_LOOP
-            for (int w = 0; w < WL; w++) cl += __popc(Ls[w] & rl[w]);
+            for (int w = 0; w < WL && cl < need_l; w++) cl += __popc(Ls[w] & rl[w]);
             keep = cl >= need_l;
           }
         }
