@@ -822,8 +822,9 @@ __device__ __forceinline__ void leaf_parents(const Params &P, const Frame &f, co
         if (act && x < WL) m = Ls[x] & rl[x] & (rl2 ? rl2[x] : FULL);
         ncand += __popc(m);
         if (!INSTR && f.compact) m &= f.s1()[x];
-        eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, rp, acc,
-                           tl);
+        if (__any_sync(FULL, m != 0u))  // a word with no leaf anywhere in the warp: skip
+          eval_leaves<INSTR>(P, f, d, R, list + base, lane, 0xffffffffu, x * 32, m, wr, rp, acc,
+                             tl);
       }
       lb.ncand[lane] = ncand;
     }
