@@ -872,6 +872,7 @@ __device__ __forceinline__ int expand_children(const Params &P, const Frame &f, 
       const uint32_t mall = act && x < WL ? Ls[x] & rl[x] : 0u;
       ncand_u += __popc(mall);
       const uint32_t m = INSTR || !f.compact ? mall : mall & f.s1()[x];
+      if (!__any_sync(FULL, m != 0u)) continue;  // no candidate in this word anywhere
       const int cnt = __popc(m);
       int incl = cnt;
 #pragma unroll
