@@ -819,6 +819,27 @@ inline unsigned warp_blocks(int64_t n_items, int sms) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
+// (r << ib) | id keys of every directed pair (warp per root): lower part from low_buf,
+// upper part from dir_idx
+__global__ void dir_sort_keys(const int64_t *__restrict__ doff, const int64_t *__restrict__ low_end,
+                              const int32_t *__restrict__ low_buf, const int32_t *__restrict__ didx,
+                              int64_t n, int ib, unsigned long long *__restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    const int64_t le = low_end[r];
+    for (int64_t i = doff[r] + lane; i < doff[r + 1]; i += 32)
+      keys[i] = ((unsigned long long)r << ib) | (unsigned long long)(i < le ? low_buf[i] : didx[i]);
+  }
+}
+
+__global__ void key_low_ids(const unsigned long long *__restrict__ keys, int64_t m, int ib,
+                            int32_t *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) out[i] = (int32_t)(keys[i] & ((1ull << ib) - 1ull));
+}
+
 // HTB of a CSR family into (off, idx, val)
 void build_htb(const int64_t *off, const int32_t *idx, int64_t n, int64_t E, DBuf<int64_t> &hoff,
                DBuf<uint32_t> &hidx, DBuf<uint32_t> &hval, int64_t &total, int64_t &max_slice,
@@ -1286,13 +1307,25 @@ void prepare(const DevGraph &g, int p, int q, const bc_config &cfg, DevStructs &
       BC_CHECK_LAUNCH();
     }
     if (s.dir2_pairs > 0) {
+      // the lower parts (ids < r, from the other endpoints' upper lists) arrive unordered;
+      // every list is ordered by one radix sort of (r, id) keys over all pairs (upper
+      // parts are already ascending and above r, so only the lower parts move)
+      int ib = 1;
+      while ((int64_t(1) << ib) < n) ib++;
+      DBuf<unsigned long long> k0, k1;
+      k0.alloc(s.dir2_pairs, st);
+      k1.alloc(s.dir2_pairs, st);
+      dir_sort_keys<<<warp_blocks(n, sms), 256, 0, st>>>(s.dir_off.p, low_end.p, low_buf.p,
+                                                         s.dir_idx.p, n, ib, k0.p);
       size_t tmp = 0;
-      BC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, low_buf.p, s.dir_idx.p,
-                                                  s.dir2_pairs, n, s.dir_off.p, low_end.p, st));
+      BC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.p, k1.p, s.dir2_pairs, 0, 2 * ib, st));
       DBuf<char> t;
       t.alloc(tmp, st);
-      BC_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, low_buf.p, s.dir_idx.p, s.dir2_pairs,
-                                                  n, s.dir_off.p, low_end.p, st));
+      BC_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tmp, k0.p, k1.p, s.dir2_pairs, 0, 2 * ib, st));
+      key_low_ids<<<blocks_for(s.dir2_pairs, 256), 256, 0, st>>>(k1.p, s.dir2_pairs, ib,
+                                                                 s.dir_idx.p);
+      BC_CHECK_LAUNCH();
+      L += 2;
     }
     L += 6;
   }
