@@ -550,7 +550,9 @@ __global__ void l1_task_totals(const int2 *__restrict__ tasks, const int64_t *lt
   const int64_t k = t - troot[r], D = doff[r + 1] - doff[r];
   const int nch = unit_first[r + 1] - unit_first[r];
   unsigned long long c = 0;
-  for (int ch = 0; ch < nch; ch++) c += aux[ubase[r] + ch * D + k];
+  const unsigned long long *col = aux + ubase[r] + k;
+#pragma unroll 8
+  for (int ch = 0; ch < nch; ch++) c += col[ch * D];  // independent loads in flight
   cnt[j] = (int64_t)c;
 }
 
@@ -567,10 +569,21 @@ __global__ void l1_cursors(const int2 *__restrict__ tasks, const int64_t *ltask,
   const int64_t k = t - troot[r], D = doff[r + 1] - doff[r];
   const int nch = unit_first[r + 1] - unit_first[r];
   unsigned long long run = (unsigned long long)roff[j];
-  for (int ch = 0; ch < nch; ch++) {
-    unsigned long long *p = aux + ubase[r] + ch * D + k;
-    const unsigned long long x = *p;
-    *p = run;
+  unsigned long long *col = aux + ubase[r] + k;
+  int ch = 0;
+  for (; ch + 8 <= nch; ch += 8) {  // eight independent loads in flight, then the prefix
+    unsigned long long x[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) x[u] = col[(ch + u) * D];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      col[(ch + u) * D] = run;
+      run += x[u];
+    }
+  }
+  for (; ch < nch; ch++) {
+    const unsigned long long x = col[ch * D];
+    col[ch * D] = run;
     run += x;
   }
 }
