@@ -19,7 +19,7 @@ timeout 900 ncu $M --log-file $o/launches_C3_63.csv python scripts/one_count.py 
 timeout 900 ncu $M --log-file $o/launches_C3_36.csv python scripts/one_count.py C3 1 3 6 > /dev/null 2>&1
 F="--set full --import-source on --clock-control none"
 timeout 900 ncu $F -k regex:enum_kernel -s 0 -c 1 -o $o/full_c5_triage -f python scripts/one_count.py C5 1 > /dev/null 2>&1
-timeout 900 ncu $F -k regex:sub_kernel -s 2 -c 1 -o $o/full_c5_sub -f python scripts/one_count.py C5 1 > /dev/null 2>&1
+timeout 900 ncu $F -k regex:sub_kernel -c 1 -o $o/full_c5_sub -f python scripts/one_count.py C5 1 > /dev/null 2>&1
 timeout 900 ncu $F -k regex:rfilter_kernel -c 1 -o $o/full_c5_rfilter -f python scripts/one_count.py C5 1 > /dev/null 2>&1
 timeout 900 ncu $F -k regex:l1_scatter -s 1 -c 1 -o $o/full_c5_l1fill -f python scripts/one_count.py C5 1 > /dev/null 2>&1
 timeout 900 ncu $F -k regex:enum_kernel -s 1 -c 1 -o $o/full_c2_enum -f python scripts/one_count.py C2 2 > /dev/null 2>&1
