@@ -218,7 +218,8 @@ int64_t bc_export_len(const bc_structs *s, int32_t what);
 int bc_export(const bc_structs *s, int32_t what, void *host_dst);
 void bc_structs_destroy(bc_structs *s);
 
-/* Drop cached device state (streams, scratch). */
+/* Hand the cached scratch of the library's per-device memory pools back to the device
+   (live graphs and structures keep their allocations). */
 void bc_shutdown(void);
 
 /* Development builds compiled with -DBC_PHASE_PROF: per-phase SM-cycle tallies of

@@ -19,11 +19,19 @@ thread_local int64_t t_h2d_bytes = 0, t_d2h_bytes = 0;
 
 namespace bc {
 
-cudaMemPool_t lib_pool(int device) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t lib_pool_if_created(int device) {
   if (device < 0 || device >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  return g_pools[device];
+}
+
+cudaMemPool_t lib_pool(int device) {
+  cudaMemPool_t *pools = g_pools;
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
   if (!pools[device]) {
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
@@ -661,7 +669,20 @@ void bc_structs_destroy(bc_structs *r) {
   if (st) cudaStreamSynchronize(st);
 }
 
-void bc_shutdown(void) {}
+void bc_shutdown(void) {
+  // hand the library pools' cached memory back to the device (graphs and structures the
+  // caller still holds keep their own allocations) and forget the reservations
+  for (int d = 0; d < 64; d++) {
+    std::lock_guard<std::mutex> lk(dev_mu(d));
+    if (!bc::lib_pool_if_created(d)) continue;
+    cudaSetDevice(d);
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(bc::lib_pool_if_created(d), 0);
+    g_pool_reserved[d] = 0;
+    g_pool_high[d] = 0;
+  }
+  cudaGetLastError();
+}
 
 int bc_debug_phase_cycles(uint64_t *out, int32_t n) {
   try {

@@ -26,6 +26,7 @@ struct DevGraph {
 // threshold UINT64_MAX so freed scratch stays cached between calls).  Private, so the
 // caching never changes the device's default pool that PyTorch or NCCL allocate from.
 cudaMemPool_t lib_pool(int device);
+cudaMemPool_t lib_pool_if_created(int device);  // null until the first allocation
 inline cudaError_t pool_malloc(void **p, size_t bytes, cudaStream_t st) {
   int d = 0;
   cudaError_t e = cudaGetDevice(&d);

@@ -143,3 +143,22 @@ def test_one_call_over_several_devices(golden, devs):
         assert sorted(rep.task_tally) == [(0, i) for i in range(want["emitted"])]
     with pytest.raises(ValueError):
         EngineConfig(devices=()).validate()
+
+
+def test_shutdown_releases_cache_and_counts_again(golden):
+    """bc_shutdown hands the library pools' cached scratch back to the device; a live graph
+    keeps working and later calls re-reserve (same counts)."""
+    from paper_2403_07858_b200 import DeviceGraph, _abi
+
+    g = synth.build_config("C4")
+    want = golden["configs"]["C4"]["(8,8)"]["hybrid"]["count"]
+    dg = DeviceGraph(g)
+    try:
+        r1, _ = dg.count_raw(8, 8)
+        _abi.load().bc_shutdown()
+        r2, _ = dg.count_raw(8, 8)
+    finally:
+        dg.close()
+    assert str(int(r1.count_lo) | (int(r1.count_hi) << 64)) == want
+    assert str(int(r2.count_lo) | (int(r2.count_hi) << 64)) == want
+    assert str(count_bicliques(g, 8, 8).count) == want
