@@ -121,3 +121,23 @@ def test_graph_csr_matches_reference_shape():
     t = transpose(g)
     assert t.u_count == 5 and t.v_count == 4
     assert np.array_equal(t.u_csr.idx, g.v_csr.idx)
+
+
+def test_integration_snippet_struct_layouts():
+    """The reference-side binding shown in INTEGRATION.md declares bc_config / bc_report
+    with the same fields, types and sizes as the library's own binding (and so the
+    header): a stale snippet would hand bc_count a short struct."""
+    import ctypes as C
+    import re
+
+    from paper_2403_07858_b200 import _abi
+
+    text = open(os.path.join(os.path.dirname(os.path.dirname(HEADER)), "INTEGRATION.md")).read()
+    ns = {"C": C}
+    for name in ("_Cfg", "_Rep"):
+        m = re.search(rf"class {name}\(C\.Structure\):.*?\n\n", text, re.S)
+        assert m, name
+        exec(m.group(0), ns)
+    for mine, theirs in ((ns["_Cfg"], _abi.BcConfig), (ns["_Rep"], _abi.BcReport)):
+        assert [(n, t) for n, t in mine._fields_] == [(n, t) for n, t in theirs._fields_]
+        assert C.sizeof(mine) == C.sizeof(theirs)
