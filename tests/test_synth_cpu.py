@@ -44,3 +44,20 @@ def test_planted_cores_are_in_the_graph():
 def test_config_fingerprints():
     for name in ("C1", "C4"):
         assert synth.build_config(name).fingerprint() == synth.FINGERPRINTS[name]
+
+
+def test_bench_cpu_calibration_chunk():
+    """bench.py's C5 CPU estimate scales a fixed chunk of roots by that chunk's measured
+    share of the offline full oracle run (profiles/r2/c5_oracle_chunks.jsonl): the chunks
+    must cover every root once and the calibration chunk must be among them."""
+    import importlib.util
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    lo, hi, t_chunk, t_full, n_chunks, threads = bench.calibration_chunk("C5")
+    assert (lo, hi) == bench.CAL_CHUNK["C5"] and 0 < t_chunk < t_full
+    assert n_chunks == 44 and threads >= 1
+    assert bench.calibration_chunk("C2") is None
