@@ -304,7 +304,13 @@ __global__ void __launch_bounds__(256) nesting_check(Params P, const Info *__res
 // ---------------------------------------------------------------------------
 // Rank-order positions inside each root's directed list (for the restricted rows): the
 // j-th entry of root r's segment after the sort is the j-th lowest-ranked member of dir2(r).
-// Keys (root << rb) | rank of every dir2 entry (warp per root): one radix sort by these
+// pos[ids[i]] = i: a vertex's position in ascending rank order
+__global__ void scatter_pos(const int32_t *__restrict__ ids, int64_t n, int64_t *__restrict__ pos) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) pos[ids[i]] = i;
+}
+
+// Keys (root << rb) | rank position of every dir2 entry (warp per root): one radix sort by these
 // orders each root's list by rank -- cheaper than a segmented sort of 44 K short segments
 __global__ void dir_rank_keys64(const int64_t *__restrict__ doff, const int32_t *__restrict__ didx,
                                 const int64_t *__restrict__ rank, int64_t n, int rb,
@@ -1260,11 +1266,30 @@ void search(const DevStructs &s, const bc_config &cfg, bc_report &out) {
           k1.alloc(D, st);
           v0.alloc(D, st);
           v1.alloc(D, st);
-          int rb = 1;  // bits of a rank (ranks are 1..n)
-          while ((int64_t(1) << rb) <= n) rb++;
+          // dense rank positions 0..n-1 of the anchors (rank overrides, e.g. a partitioned
+          // count's global ranks, can be any distinct int64s): one small sort of the ranks
+          DBuf<int64_t> dpos, rk2;
+          DBuf<int32_t> vid, vid2;
+          dpos.alloc(n, st);
+          rk2.alloc(n, st);
+          vid.alloc(n, st);
+          vid2.alloc(n, st);
+          iota32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vid.p, n);
+          {
+            size_t t0 = 0;
+            BC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t0, s.rank.p, rk2.p, vid.p, vid2.p, n,
+                                                    0, 64, st));
+            DBuf<char> tb0;
+            tb0.alloc(t0, st);
+            BC_CUDA(cub::DeviceRadixSort::SortPairs(tb0.p, t0, s.rank.p, rk2.p, vid.p, vid2.p, n,
+                                                    0, 64, st));
+          }
+          scatter_pos<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vid2.p, n, dpos.p);
+          int rb = 1;  // bits of a rank position (< n)
+          while ((int64_t(1) << rb) < n) rb++;
           int nb = 1;  // bits of a root id
           while ((int64_t(1) << nb) < n) nb++;
-          dir_rank_keys64<<<sms * 8, 256, 0, st>>>(s.dir_off.p, s.dir_idx.p, s.rank.p, n, rb, k0.p,
+          dir_rank_keys64<<<sms * 8, 256, 0, st>>>(s.dir_off.p, s.dir_idx.p, dpos.p, n, rb, k0.p,
                                                    v0.p);
           DBuf<int64_t> seg_end;
           seg_end.alloc(n, st);

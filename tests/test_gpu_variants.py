@@ -330,3 +330,30 @@ def test_forced_triage_configs(golden, name, p, q, kw):
     assert str(rep.count) == want["count"]
     assert rep.batches_executed == want["batches"]
     assert rep.tasks_emitted == want["emitted"]
+
+
+@pytest.mark.parametrize("kw", TRIAGE_PATHS[:3])
+def test_rank_override_any_values_on_restricted_rows(kw):
+    """A rank override (a partitioned count passes the full graph's ranks, partition.py:
+    246-249) may hold any distinct int64s: the restricted rows' rank positions must follow
+    their order, not their magnitude.  Order-preserving rescalings of the reference rank
+    (large, negative) give the reference's counts, batches and per-task counts."""
+    rng = np.random.default_rng(41)
+    for i in range(4):
+        g = synth.random_bipartite(int(rng.integers(60, 110)), int(rng.integers(60, 110)),
+                                   float(rng.uniform(0.2, 0.4)), int(rng.integers(1 << 30)))
+        p, q = int(rng.integers(5, 8)), int(rng.integers(2, 5))
+        prep = O.Prepared(g, p, q, anchor="U")
+        rank = prep.export(O.X_RANK).astype(np.int64)
+        want = O.count(g, p, q, anchor="U", per_task=True)
+        dg = DeviceGraph(g)
+        try:
+            for rk in (rank * 1_000_003 + 7, rank - 10**15):
+                rep, per_task = dg.count_raw(p, q, EngineConfig(anchor="U", **kw), rank=rk,
+                                             task_counts=True)
+                got = int(rep.count_lo) | (int(rep.count_hi) << 64)
+                assert got == want.count, (i, p, q, kw)
+                assert per_task == want.task_counts, (i, p, q, kw)
+                assert rep.batches_executed == want.batches_executed, (i, p, q, kw)
+        finally:
+            dg.close()
