@@ -313,14 +313,14 @@ __global__ void scatter_pos(const int32_t *__restrict__ ids, int64_t n, int64_t 
 // Keys (root << rb) | rank position of every dir2 entry (warp per root): one radix sort by these
 // orders each root's list by rank -- cheaper than a segmented sort of 44 K short segments
 __global__ void dir_rank_keys64(const int64_t *__restrict__ doff, const int32_t *__restrict__ didx,
-                                const int64_t *__restrict__ rank, int64_t n, int rb,
+                                const int64_t *__restrict__ rpos_of, int64_t n, int rb,
                                 unsigned long long *__restrict__ keys, int32_t *__restrict__ vals) {
   const int lane = lane_id();
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = gw; r < n; r += nw)
     for (int64_t i = doff[r] + lane; i < doff[r + 1]; i += 32) {
-      keys[i] = ((unsigned long long)r << rb) | (unsigned long long)rank[didx[i]];
+      keys[i] = ((unsigned long long)r << rb) | (unsigned long long)rpos_of[didx[i]];
       vals[i] = (int32_t)i;
     }
 }
